@@ -1,0 +1,597 @@
+// C ABI (include/warpstar.h): context lifetime, value upload, pass launch,
+// result download, and the legacy per-level shims.
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ws_internal.h"
+
+struct ws_ctx {
+    ws::Context c;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_err_pin = -1;
+
+template <class F>
+int guarded(F&& f)
+{
+    try {
+        f();
+        return WS_OK;
+    } catch (const ws::Error& e) {
+        g_err = e.what();
+        g_err_pin = e.pin;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return WS_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return WS_ERR_CUDA;
+    }
+}
+
+void check_corner(const ws::Context& c, int corner, int n = 1)
+{
+    if (corner < 0 || n < 1 || corner + n > (int)c.corners.size())
+        throw ws::Error(WS_ERR_VALUE, "corner index out of range");
+}
+
+int64_t value_len(const ws::Context& c, int field)
+{
+    const ws::Topo& t = c.t;
+    switch (field) {
+    case WS_V_MEM_RES: case WS_V_MEM_CAP: return 4ll * t.M;
+    case WS_V_ROOT_CAP: return 4ll * t.N;
+    case WS_V_LUT_T: return c.lut_t_len;
+    case WS_V_PI_ARRIVAL: case WS_V_PI_SLEW: return 4ll * t.I;
+    case WS_V_EP_REQUIRED: return 4ll * t.E;
+    default: throw ws::Error(WS_ERR_VALUE, "unknown value field");
+    }
+}
+
+double* value_ptr(ws::Corner& d, int field)
+{
+    switch (field) {
+    case WS_V_MEM_RES: return d.mem_res;
+    case WS_V_MEM_CAP: return d.mem_cap;
+    case WS_V_ROOT_CAP: return d.root_cap;
+    case WS_V_LUT_T: return d.lut_t_flat;
+    case WS_V_PI_ARRIVAL: return d.pi_arrival;
+    case WS_V_PI_SLEW: return d.pi_slew;
+    case WS_V_EP_REQUIRED: return d.ep_required;
+    default: throw ws::Error(WS_ERR_VALUE, "unknown value field");
+    }
+}
+
+int64_t state_len(const ws::Context& c, int field)
+{
+    const ws::Topo& t = c.t;
+    switch (field) {
+    case WS_F_LOAD: case WS_F_NET_DELAY: case WS_F_IMPULSE: case WS_F_SLEW: case WS_F_ARRIVAL:
+    case WS_F_REQUIRED: case WS_F_SLACK: return 4ll * t.P;
+    case WS_F_ARC_DELAY: return 4ll * t.A;
+    case WS_F_LSE_ARRIVAL: case WS_F_ADJOINT: return 2ll * t.P;
+    case WS_F_ARC_WEIGHTS: case WS_F_D_ARC: return 2ll * t.A;
+    case WS_F_D_EDGE: return 2ll * t.M;
+    case WS_F_SUMMARY: return 3;
+    default: throw ws::Error(WS_ERR_VALUE, "unknown state field");
+    }
+}
+
+double* state_ptr(ws::Corner& d, int field)
+{
+    switch (field) {
+    case WS_F_LOAD: return d.load;
+    case WS_F_NET_DELAY: return d.net_delay;
+    case WS_F_IMPULSE: return d.impulse;
+    case WS_F_SLEW: return d.slew;
+    case WS_F_ARRIVAL: return d.arrival;
+    case WS_F_REQUIRED: return d.required;
+    case WS_F_SLACK: return d.slack;
+    case WS_F_ARC_DELAY: return d.arc_delay;
+    case WS_F_LSE_ARRIVAL: return d.lse_at;
+    case WS_F_ARC_WEIGHTS: return d.weights;
+    case WS_F_D_ARC: return d.d_arc;
+    case WS_F_D_EDGE: return d.d_edge;
+    case WS_F_ADJOINT: return d.adjoint;
+    case WS_F_SUMMARY: return d.summary;
+    default: throw ws::Error(WS_ERR_VALUE, "unknown state field");
+    }
+}
+
+cudaStream_t as_stream(void* s, cudaStream_t dflt) { return s ? static_cast<cudaStream_t>(s) : dflt; }
+
+}  // namespace
+
+namespace ws {
+
+void alloc_corner(Context& ctx, CornerSlot& cs)
+{
+    const Topo& t = ctx.t;
+    Arena& ar = ctx.val_mem;
+    Corner& d = cs.d;
+    d.mem_res = ar.alloc<double>(4 * (size_t)t.M);
+    d.mem_cap = ar.alloc<double>(4 * (size_t)t.M);
+    d.root_cap = ar.alloc<double>(4 * (size_t)t.N);
+    d.lut_t_flat = ar.alloc<double>((size_t)ctx.lut_t_len);
+    d.pi_arrival = ar.alloc<double>(4 * (size_t)t.I);
+    d.pi_slew = ar.alloc<double>(4 * (size_t)t.I);
+    d.ep_required = ar.alloc<double>(4 * (size_t)t.E);
+    d.load = ar.alloc<double>(4 * (size_t)t.P);
+    d.net_delay = ar.alloc<double>(4 * (size_t)t.P);
+    d.impulse = ar.alloc<double>(4 * (size_t)t.P);
+    d.slew = ar.alloc<double>(4 * (size_t)t.P);
+    d.arrival = ar.alloc<double>(4 * (size_t)t.P);
+    d.required = ar.alloc<double>(4 * (size_t)t.P);
+    d.slack = ar.alloc<double>(4 * (size_t)t.P);
+    d.arc_delay = ar.alloc<double>(4 * (size_t)t.A);
+    d.lse_at = ar.alloc<double>(2 * (size_t)t.P);
+    d.weights = ar.alloc<double>(2 * (size_t)t.A);
+    d.d_arc = ar.alloc<double>(2 * (size_t)t.A);
+    d.d_edge = ar.alloc<double>(2 * (size_t)t.M);
+    d.adjoint = ar.alloc<double>(2 * (size_t)t.P);
+    // tree-net RC scratch only when the design has RC trees (or w != 8 is
+    // requested later: allocated lazily then)
+    d.mem_buf = nullptr;
+    d.mem_dbuf = nullptr;
+    const int nl = ctx.tns_plan ? std::max(1, ctx.tns_plan->n_leaves) : 1;
+    d.red_tmp = ar.alloc<double>(3 * (size_t)(2 * nl));
+    d.summary = ar.alloc<double>(4);
+    // arrays that are not fully rewritten by every pass start defined
+    WS_CUDA(cudaMemset(d.arc_delay, 0, sizeof(double) * 4 * (size_t)std::max(t.A, 1)));
+    WS_CUDA(cudaMemset(d.weights, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));
+    WS_CUDA(cudaMemset(d.d_arc, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));
+    WS_CUDA(cudaMemset(d.d_edge, 0, sizeof(double) * 2 * (size_t)std::max(t.M, 1)));
+    WS_CUDA(cudaMemset(d.lse_at, 0, sizeof(double) * 2 * (size_t)std::max(t.P, 1)));
+    WS_CUDA(cudaMemset(d.adjoint, 0, sizeof(double) * 2 * (size_t)std::max(t.P, 1)));
+    WS_CUDA(cudaMemset(d.slack, 0, sizeof(double) * 4 * (size_t)std::max(t.P, 1)));
+    WS_CUDA(cudaMemset(d.summary, 0, sizeof(double) * 4));
+}
+
+void ensure_tree_scratch(Context& ctx)
+{
+    for (auto& cs : ctx.corners)
+        if (!cs.d.mem_buf) {
+            cs.d.mem_buf = ctx.val_mem.alloc<double>(4 * (size_t)ctx.t.M);
+            cs.d.mem_dbuf = ctx.val_mem.alloc<double>(4 * (size_t)ctx.t.M);
+        }
+    std::vector<Corner> v;
+    for (auto& cs : ctx.corners) v.push_back(cs.d);
+    WS_CUDA(cudaMemcpy(ctx.d_corners, v.data(), sizeof(Corner) * v.size(), cudaMemcpyHostToDevice));
+}
+
+void upload_values(Context& ctx, int corner, const ws_design_desc* d)
+{
+    Corner& c = ctx.corners[corner].d;
+    const Topo& t = ctx.t;
+    auto up = [&](double* dst, const double* src, size_t n) {
+        if (n) WS_CUDA(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyHostToDevice));
+    };
+    up(c.mem_res, d->mem_res, 4 * (size_t)t.M);
+    up(c.mem_cap, d->mem_cap, 4 * (size_t)t.M);
+    up(c.root_cap, d->root_cap, 4 * (size_t)t.N);
+    up(c.lut_t_flat, d->lut_t_flat, (size_t)ctx.lut_t_len);
+    up(c.pi_arrival, d->pi_arrival, 4 * (size_t)t.I);
+    up(c.pi_slew, d->pi_slew, 4 * (size_t)t.I);
+    up(c.ep_required, d->ep_required, 4 * (size_t)t.E);
+}
+
+}  // namespace ws
+
+extern "C" {
+
+int ws_abi_version(void) { return WS_ABI_VERSION; }
+const char* ws_last_error(void) { return g_err.c_str(); }
+int64_t ws_last_error_pin(void) { return g_err_pin; }
+
+int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
+{
+    ws_ctx* h = nullptr;
+    int rc = guarded([&] {
+        if (!d || !out) throw ws::Error(WS_ERR_VALUE, "null argument");
+        if (n_corners < 1) throw ws::Error(WS_ERR_VALUE, "n_corners must be >= 1");
+        if (!(d->clock_period > 0.0)) throw ws::Error(WS_ERR_VALUE, "clock_period must be positive");
+        h = new ws_ctx();
+        ws::Context& c = h->c;
+        c.clock_period = d->clock_period;
+        WS_CUDA(cudaStreamCreateWithFlags(&c.s_main, cudaStreamNonBlocking));
+        WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamNonBlocking));
+        ws::build_topology(c, d);
+        ws::summary_plan_init(c);
+        c.corners.resize(n_corners);
+        for (auto& cs : c.corners) ws::alloc_corner(c, cs);
+        for (int k = 0; k < n_corners; k++) ws::upload_values(c, k, d);
+        c.d_corners = c.topo_mem.alloc<ws::Corner>(n_corners);
+        int any_tree = 0;
+        for (int v : c.lv_tree_host) any_tree |= v;
+        if (any_tree) ws::ensure_tree_scratch(c);
+        std::vector<ws::Corner> v;
+        for (auto& cs : c.corners) v.push_back(cs.d);
+        WS_CUDA(cudaMemcpy(c.d_corners, v.data(), sizeof(ws::Corner) * v.size(), cudaMemcpyHostToDevice));
+        WS_CUDA(cudaDeviceSynchronize());
+    });
+    if (rc != WS_OK) {
+        if (h) ws_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return WS_OK;
+}
+
+void ws_destroy(ws_ctx* h)
+{
+    if (!h) return;
+    ws::Context& c = h->c;
+    cudaDeviceSynchronize();
+    for (auto& g : c.graphs) cudaGraphExecDestroy(g.exec);
+    for (auto e : c.events) cudaEventDestroy(e);
+    ws::summary_plan_free(c);
+    c.val_mem.release();
+    c.topo_mem.release();
+    c.scratch.release();
+    if (c.s_main) cudaStreamDestroy(c.s_main);
+    if (c.s_grad) cudaStreamDestroy(c.s_grad);
+    delete h;
+}
+
+int ws_dims(ws_ctx* h, int64_t* dims)
+{
+    return guarded([&] {
+        if (!h || !dims) throw ws::Error(WS_ERR_VALUE, "null argument");
+        const ws::Topo& t = h->c.t;
+        const int64_t v[WS_DIMS_LEN] = {t.P, t.N, t.M, t.A, t.I, t.E, t.L, t.NL,
+                                        (int64_t)h->c.corners.size(), t.max_in, t.max_m};
+        memcpy(dims, v, sizeof(v));
+    });
+}
+
+int64_t ws_topology_len(ws_ctx* h, int field)
+{
+    int64_t n = -1;
+    int rc = guarded([&] {
+        if (!h) throw ws::Error(WS_ERR_VALUE, "null context");
+        n = ws::topo_field_len(h->c, field);
+    });
+    return rc == WS_OK ? n : -1;
+}
+
+int ws_get_topology(ws_ctx* h, int field, int64_t* dst)
+{
+    return guarded([&] {
+        if (!h || !dst) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::topo_field_to_host(h->c, field, dst);
+    });
+}
+
+int ws_set_values(ws_ctx* h, int corner, int field, const double* src, int src_on_device, void* stream)
+{
+    return guarded([&] {
+        if (!h || !src) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        const int64_t n = value_len(c, field);
+        cudaStream_t s = as_stream(stream, c.s_main);
+        if (n)
+            WS_CUDA(cudaMemcpyAsync(value_ptr(c.corners[corner].d, field), src, (size_t)n * sizeof(double),
+                                    src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        if (!stream) WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_perturb_values(ws_ctx* h, int corner, int base_corner, uint64_t seed, double sigma,
+                      void* stream)
+{
+    return guarded([&] {
+        if (!h) throw ws::Error(WS_ERR_VALUE, "null context");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        check_corner(c, base_corner);
+        if (!(sigma >= 0.0 && sigma < 1.0 / 3.0))
+            throw ws::Error(WS_ERR_VALUE, "sigma must be in [0, 1/3) so every factor stays positive");
+        cudaStream_t s = as_stream(stream, c.s_main);
+        if (corner != base_corner) {
+            const ws::Corner& a = c.corners[base_corner].d;
+            const ws::Corner& b = c.corners[corner].d;
+            auto cp = [&](double* dst, const double* src, size_t n) {
+                if (n) WS_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            };
+            cp(b.lut_t_flat, a.lut_t_flat, (size_t)c.lut_t_len);
+            cp(b.pi_arrival, a.pi_arrival, 4 * (size_t)c.t.I);
+            cp(b.pi_slew, a.pi_slew, 4 * (size_t)c.t.I);
+            cp(b.ep_required, a.ep_required, 4 * (size_t)c.t.E);
+        }
+        ws::launch_perturb(c, corner, base_corner, (unsigned long long)seed, sigma, s);
+        if (!stream) WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, int loss_kind,
+           int reduce_width, int granularity, void* stream, void* stream_grad)
+{
+    return guarded([&] {
+        if (!h) throw ws::Error(WS_ERR_VALUE, "null context");
+        ws::Context& c = h->c;
+        check_corner(c, corner0, n_corners);
+        if ((flags & (WS_RUN_LSE | WS_RUN_GRAD)) && !(gamma > 0.0 && gamma < __builtin_huge_val()))
+            throw ws::Error(WS_ERR_VALUE, "gamma must be positive and finite");
+        if (loss_kind != WS_LOSS_HINGE && loss_kind != WS_LOSS_SOFTPLUS)
+            throw ws::Error(WS_ERR_VALUE, "unknown loss kind");
+        if (reduce_width < 1 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
+            throw ws::Error(WS_ERR_VALUE, "reduce_width must be a power of two in [1, 32]");
+        if (granularity < 1) throw ws::Error(WS_ERR_VALUE, "granularity must be >= 1");
+        if (reduce_width != 8) ws::ensure_tree_scratch(c);
+        cudaStream_t s = as_stream(stream, c.s_main);
+        cudaStream_t g = as_stream(stream_grad, c.s_grad);
+        if (flags & WS_RUN_GRAPH) {
+            const unsigned key = flags & ~WS_RUN_GRAPH;
+            cudaGraphExec_t exec = nullptr;
+            for (auto& e : c.graphs)
+                if (e.key == key && e.c0 == corner0 && e.nc == n_corners && e.gamma == gamma &&
+                    e.loss == loss_kind && e.gran == granularity * 64 + reduce_width) exec = e.exec;
+            if (!exec) {
+                cudaStream_t cap;
+                WS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                cudaStream_t capg;
+                WS_CUDA(cudaStreamCreateWithFlags(&capg, cudaStreamNonBlocking));
+                WS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+                ws::run_pass(c, corner0, n_corners, key, gamma, loss_kind, granularity, cap, capg,
+                             reduce_width, c.d_corners);
+                cudaGraph_t graph;
+                WS_CUDA(cudaStreamEndCapture(cap, &graph));
+                WS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+                WS_CUDA(cudaGraphDestroy(graph));
+                cudaStreamDestroy(cap);
+                cudaStreamDestroy(capg);
+                c.graphs.push_back({key, corner0, n_corners, gamma, loss_kind,
+                                    granularity * 64 + reduce_width, exec});
+                c.graph_launches.push_back(c.launches_last_run);
+            }
+            int cnt = 0;
+            for (size_t i = 0; i < c.graphs.size(); i++)
+                if (c.graphs[i].exec == exec) cnt = c.graph_launches[i];
+            WS_CUDA(cudaGraphLaunch(exec, s));
+            c.launches_last_run = cnt;
+        } else {
+            ws::run_pass(c, corner0, n_corners, flags, gamma, loss_kind, granularity, s, g,
+                         reduce_width, c.d_corners);
+        }
+        if (flags & WS_RUN_HARD)
+            for (int k = 0; k < n_corners; k++) c.corners[corner0 + k].has_lse = false;
+        if (flags & WS_RUN_LSE)
+            for (int k = 0; k < n_corners; k++) c.corners[corner0 + k].has_lse = true;
+        if (!stream) WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_set_state(ws_ctx* h, int corner, int field, const double* src, int src_on_device, void* stream)
+{
+    return guarded([&] {
+        if (!h || !src) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        const int64_t n = state_len(c, field);
+        cudaStream_t s = as_stream(stream, c.s_main);
+        if (n)
+            WS_CUDA(cudaMemcpyAsync(state_ptr(c.corners[corner].d, field), src, (size_t)n * sizeof(double),
+                                    src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        if (!stream) WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_get(ws_ctx* h, int corner, int field, double* dst, int dst_on_device, void* stream)
+{
+    return guarded([&] {
+        if (!h || !dst) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        const int64_t n = state_len(c, field);
+        cudaStream_t s = as_stream(stream, c.s_main);
+        if (n)
+            WS_CUDA(cudaMemcpyAsync(dst, state_ptr(c.corners[corner].d, field), (size_t)n * sizeof(double),
+                                    dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_device_ptr(ws_ctx* h, int corner, int field, void** dptr, int64_t* n_elems)
+{
+    return guarded([&] {
+        if (!h || !dptr) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        *dptr = state_ptr(c.corners[corner].d, field);
+        if (n_elems) *n_elems = state_len(c, field);
+    });
+}
+
+int ws_value_ptr(ws_ctx* h, int corner, int field, void** dptr, int64_t* n_elems)
+{
+    return guarded([&] {
+        if (!h || !dptr) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        *dptr = value_ptr(c.corners[corner].d, field);
+        if (n_elems) *n_elems = value_len(c, field);
+    });
+}
+
+int ws_summary(ws_ctx* h, int corner, double* out, void* stream)
+{
+    return guarded([&] {
+        if (!h || !out) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        cudaStream_t s = as_stream(stream, c.s_main);
+        WS_CUDA(cudaMemcpyAsync(out, c.corners[corner].d.summary, 3 * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_last_launch_count(ws_ctx* h) { return h ? h->c.launches_last_run : -1; }
+
+// ---------------------------------------------------------------------------
+// legacy per-level shims
+
+namespace {
+
+struct ShimArena {
+    ws::Arena ar;
+    ~ShimArena() { ar.release(); }
+    int* i32(const int64_t* src, int64_t n)
+    {
+        std::vector<int> v((size_t)std::max<int64_t>(n, 1));
+        for (int64_t i = 0; i < n; i++) {
+            if (src[i] < INT32_MIN || src[i] > INT32_MAX)
+                throw ws::Error(WS_ERR_VALUE, "index exceeds the int32 range");
+            v[(size_t)i] = (int)src[i];
+        }
+        int* d = ar.alloc<int>(v.size());
+        WS_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+        return d;
+    }
+    double* f64(const double* src, int64_t n)
+    {
+        double* d = ar.alloc<double>((size_t)std::max<int64_t>(n, 1));
+        if (n) WS_CUDA(cudaMemcpy(d, src, (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+        return d;
+    }
+    ws::Corner* corner(const ws::Corner& c)
+    {
+        ws::Corner* d = ar.alloc<ws::Corner>(1);
+        WS_CUDA(cudaMemcpy(d, &c, sizeof(c), cudaMemcpyHostToDevice));
+        return d;
+    }
+};
+
+void back(double* dst, const double* src, int64_t n)
+{
+    if (n) WS_CUDA(cudaMemcpy(dst, src, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+
+int ws_rc_level(int64_t n_lv, const int64_t* nets, int64_t n_nets, const int64_t* net_ptr,
+                const int64_t* net_root, const double* root_cap, int64_t n_mem,
+                const int64_t* mem_pin, const int64_t* mem_parent_loc, const double* mem_res,
+                const double* mem_cap, int64_t n_pins, const int64_t* root_net_of_pin,
+                double* load, double* net_delay, double* impulse, int reduce_width)
+{
+    return guarded([&] {
+        if (reduce_width < 1 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
+            throw ws::Error(WS_ERR_VALUE, "reduce_width must be a power of two in [1, 32]");
+        ShimArena sa;
+        ws::Topo t{};
+        t.N = (int)n_nets; t.M = (int)n_mem; t.P = (int)n_pins;
+        t.net_ptr = sa.i32(net_ptr, n_nets + 1);
+        t.net_root = sa.i32(net_root, n_nets);
+        t.mem_pin = sa.i32(mem_pin, n_mem);
+        t.mem_parent_loc = sa.i32(mem_parent_loc, n_mem);
+        t.root_net_of_pin = sa.i32(root_net_of_pin, n_pins);
+        std::vector<int64_t> tree((size_t)std::max<int64_t>(n_nets, 1), 0);
+        for (int64_t n = 0; n < n_nets; n++)
+            for (int64_t f = net_ptr[n]; f < net_ptr[n + 1]; f++)
+                if (mem_parent_loc[f] > 0) tree[(size_t)n] = 1;
+        t.net_tree = sa.i32(tree.data(), n_nets);
+        int* list = sa.i32(nets, n_lv);
+        ws::Corner c{};
+        c.root_cap = sa.f64(root_cap, 4 * n_nets);
+        c.mem_res = sa.f64(mem_res, 4 * n_mem);
+        c.mem_cap = sa.f64(mem_cap, 4 * n_mem);
+        c.load = sa.f64(load, 4 * n_pins);
+        c.net_delay = sa.f64(net_delay, 4 * n_pins);
+        c.impulse = sa.f64(impulse, 4 * n_pins);
+        c.mem_buf = sa.ar.alloc<double>(4 * (size_t)std::max<int64_t>(n_mem, 1));
+        c.mem_dbuf = sa.ar.alloc<double>(4 * (size_t)std::max<int64_t>(n_mem, 1));
+        ws::launch_rc_list(t, sa.corner(c), list, (int)n_lv, reduce_width, 0);
+        WS_CUDA(cudaDeviceSynchronize());
+        back(load, c.load, 4 * n_pins);
+        back(net_delay, c.net_delay, 4 * n_pins);
+        back(impulse, c.impulse, 4 * n_pins);
+    });
+}
+
+int ws_forward_level(int64_t n_lv, const int64_t* nets, int64_t n_nets, const int64_t* net_ptr,
+                     const int64_t* net_root, const int64_t* root_kind, int64_t n_mem,
+                     const int64_t* mem_pin, const int64_t* net_in_ptr, const int64_t* net_in_arc,
+                     int64_t n_arcs, const int64_t* arc_from, const int64_t* arc_dlut,
+                     const int64_t* arc_slut, int64_t n_luts, const int64_t* lut_s_ptr,
+                     const int64_t* lut_l_ptr, const int64_t* lut_t_ptr, const double* lut_s_flat,
+                     const double* lut_l_flat, const double* lut_t_flat, int64_t n_pins,
+                     const double* load, const double* net_delay, const double* impulse,
+                     double* slew, double* arrival, double* arc_delay)
+{
+    return guarded([&] {
+        ShimArena sa;
+        ws::Topo t{};
+        t.N = (int)n_nets; t.M = (int)n_mem; t.P = (int)n_pins; t.A = (int)n_arcs; t.NL = (int)n_luts;
+        t.lv_nets = sa.i32(nets, n_lv);
+        t.net_ptr = sa.i32(net_ptr, n_nets + 1);
+        t.net_root = sa.i32(net_root, n_nets);
+        t.root_kind = sa.i32(root_kind, n_nets);
+        t.mem_pin = sa.i32(mem_pin, n_mem);
+        t.net_in_ptr = sa.i32(net_in_ptr, n_nets + 1);
+        const int64_t n_in = n_nets > 0 ? net_in_ptr[n_nets] : 0;
+        t.net_in_arc = sa.i32(net_in_arc, n_in);
+        t.arc_from = sa.i32(arc_from, n_arcs);
+        t.arc_dlut = sa.i32(arc_dlut, 4 * n_arcs);
+        t.arc_slut = sa.i32(arc_slut, 4 * n_arcs);
+        t.lut_s_ptr = sa.i32(lut_s_ptr, n_luts + 1);
+        t.lut_l_ptr = sa.i32(lut_l_ptr, n_luts + 1);
+        t.lut_t_ptr = sa.i32(lut_t_ptr, n_luts + 1);
+        const int64_t sl = n_luts ? lut_s_ptr[n_luts] : 0, ll = n_luts ? lut_l_ptr[n_luts] : 0,
+                      tl = n_luts ? lut_t_ptr[n_luts] : 0;
+        t.lut_s_flat = sa.f64(lut_s_flat, sl);
+        t.lut_l_flat = sa.f64(lut_l_flat, ll);
+        ws::Corner c{};
+        c.lut_t_flat = sa.f64(lut_t_flat, tl);
+        c.load = sa.f64(load, 4 * n_pins);
+        c.net_delay = sa.f64(net_delay, 4 * n_pins);
+        c.impulse = sa.f64(impulse, 4 * n_pins);
+        c.slew = sa.f64(slew, 4 * n_pins);
+        c.arrival = sa.f64(arrival, 4 * n_pins);
+        c.arc_delay = sa.f64(arc_delay, 4 * n_arcs);
+        ws::launch_fwd_list(t, sa.corner(c), (int)n_lv, (int)sl, (int)ll, (int)tl, 0);
+        WS_CUDA(cudaDeviceSynchronize());
+        back(slew, c.slew, 4 * n_pins);
+        back(arrival, c.arrival, 4 * n_pins);
+        back(arc_delay, c.arc_delay, 4 * n_arcs);
+    });
+}
+
+int ws_backward_level(int64_t n_lv, const int64_t* nets, int64_t n_nets, const int64_t* net_ptr,
+                      const int64_t* net_root, int64_t n_mem, const int64_t* mem_pin,
+                      const int64_t* mem_out_ptr, const int64_t* mem_out_arc, int64_t n_arcs,
+                      const int64_t* arc_to, int64_t n_pins, const double* net_delay,
+                      double* required, const double* arc_delay)
+{
+    return guarded([&] {
+        ShimArena sa;
+        ws::Topo t{};
+        t.N = (int)n_nets; t.M = (int)n_mem; t.P = (int)n_pins; t.A = (int)n_arcs;
+        t.lv_nets = sa.i32(nets, n_lv);
+        t.net_ptr = sa.i32(net_ptr, n_nets + 1);
+        t.net_root = sa.i32(net_root, n_nets);
+        t.mem_pin = sa.i32(mem_pin, n_mem);
+        t.mem_out_ptr = sa.i32(mem_out_ptr, n_mem + 1);
+        const int64_t n_out = n_mem > 0 ? mem_out_ptr[n_mem] : 0;
+        t.mem_out_arc = sa.i32(mem_out_arc, n_out);
+        t.arc_to = sa.i32(arc_to, n_arcs);
+        ws::Corner c{};
+        c.net_delay = sa.f64(net_delay, 4 * n_pins);
+        c.required = sa.f64(required, 4 * n_pins);
+        c.arc_delay = sa.f64(arc_delay, 4 * n_arcs);
+        ws::launch_bwd_list(t, sa.corner(c), (int)n_lv, 0);
+        WS_CUDA(cudaDeviceSynchronize());
+        back(required, c.required, 4 * n_pins);
+    });
+}
+
+}  // extern "C"

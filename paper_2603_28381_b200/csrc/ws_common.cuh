@@ -1,0 +1,112 @@
+// Shared device-side definitions for the B200 STA engine (sm_100a).
+//
+// Numerics contract: compiled with -fmad=false so no a*b+c is contracted to
+// an FMA (the reference builds with -ffp-contract=off, pkg/setup.py:21-23);
+// double '/' and sqrt are IEEE correctly rounded on the device, so the hard
+// pass reproduces the reference bit for bit.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define WS_FULL 0xffffffffu
+
+namespace ws {
+
+constexpr int ROOT_ARC = 0, ROOT_PI = 1, ROOT_FEED = 2;
+
+// Topology: int32 indices, shared by every corner.
+struct Topo {
+    int P, N, M, A, I, E, L, NL;     // pins nets members arcs PIs endpoints levels luts
+    int n_free;                      // pins in no net
+    int max_in, max_m;
+    // FlatDesign arrays (flatten.py:83-136)
+    int *net_ptr, *net_root, *root_kind, *mem_pin, *mem_parent_loc, *mem_net, *mem_local;
+    int *arc_from, *arc_to, *arc_dlut, *arc_slut;
+    int *net_in_ptr, *net_in_arc, *mem_out_ptr, *mem_out_arc;
+    int *member_of_pin, *root_net_of_pin, *pi_pin, *ep_pin;
+    int *net_m, *net_a, *net_o;
+    uint8_t *is_endpoint;
+    int *lut_s_ptr, *lut_l_ptr, *lut_t_ptr;
+    double *lut_s_flat, *lut_l_flat;
+    // level schedule (flatten.py:31-80): lv_nets = nets sorted by (level, id)
+    int *level_of, *lv_ptr, *lv_nets;
+    // derived work lists
+    int *net_tree;                   // 1 if any member has a non-root parent
+    int *pin_ep_ptr, *pin_ep_idx;    // endpoint entries grouped by pin (stable)
+    int *pin_pi;                     // pin -> PI index or -1
+    int *pin_out_ptr, *pin_out_arc;  // arcs grouped by source pin (all pins)
+    int *free_pins;                  // pins that belong to no net (n_free)
+    int *nonmem_src;                 // non-member pins that source arcs
+    int n_nonmem_src;
+};
+
+// Values and state of one corner.  (P,4) arrays are row-major 32-byte
+// records, exactly the reference's TimingState layout (sta.py:41-48).
+struct Corner {
+    // values (what a corner / a placement step changes)
+    double *mem_res, *mem_cap, *root_cap, *lut_t_flat, *pi_arrival, *pi_slew, *ep_required;
+    // TimingState
+    double *load, *net_delay, *impulse, *slew, *arrival, *required, *slack, *arc_delay;
+    // GradientState (late cols only; diff.py:61-72)
+    double *lse_at, *weights, *d_arc, *d_edge, *adjoint;
+    // scratch for tree nets (RC fold) and the summary reductions
+    double *mem_buf, *mem_dbuf;
+    double *red_tmp;   // pairwise-sum node values
+    double *summary;   // [tns, wns, loss]
+};
+
+struct LutView {
+    const int *s_ptr, *l_ptr, *t_ptr;
+    const double *s, *l, *t;
+};
+
+// _kernels.pyx:15-81 / sta.py:79-113: upper_bound-1 clamped to [0,n-2],
+// fraction clamped to [0,1], 1-point axes are constants.  Same operation
+// order as the reference; no FMA (-fmad=false).
+__device__ __forceinline__ double lut_interp(const LutView& L, int lut, double qs, double ql)
+{
+    const int s0 = L.s_ptr[lut], nS = L.s_ptr[lut + 1] - s0;
+    const int l0 = L.l_ptr[lut], nL = L.l_ptr[lut + 1] - l0;
+    const int t0 = L.t_ptr[lut];
+    int si, li, si2, li2;
+    double st, lt;
+    if (nS > 1) {
+        int lo = 0, hi = nS;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (L.s[s0 + mid] <= qs) lo = mid + 1; else hi = mid;
+        }
+        si = lo - 1;
+        if (si < 0) si = 0; else if (si > nS - 2) si = nS - 2;
+        st = (qs - L.s[s0 + si]) / (L.s[s0 + si + 1] - L.s[s0 + si]);
+        if (st < 0.0) st = 0.0; else if (st > 1.0) st = 1.0;
+        si2 = si + 1;
+    } else { si = 0; st = 0.0; si2 = 0; }
+    if (nL > 1) {
+        int lo = 0, hi = nL;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (L.l[l0 + mid] <= ql) lo = mid + 1; else hi = mid;
+        }
+        li = lo - 1;
+        if (li < 0) li = 0; else if (li > nL - 2) li = nL - 2;
+        lt = (ql - L.l[l0 + li]) / (L.l[l0 + li + 1] - L.l[l0 + li]);
+        if (lt < 0.0) lt = 0.0; else if (lt > 1.0) lt = 1.0;
+        li2 = li + 1;
+    } else { li = 0; lt = 0.0; li2 = 0; }
+    const double v0 = __dadd_rn(__dmul_rn(1.0 - lt, L.t[t0 + si * nL + li]),
+                                __dmul_rn(lt, L.t[t0 + si * nL + li2]));
+    const double v1 = __dadd_rn(__dmul_rn(1.0 - lt, L.t[t0 + si2 * nL + li]),
+                                __dmul_rn(lt, L.t[t0 + si2 * nL + li2]));
+    return __dadd_rn(__dmul_rn(1.0 - st, v0), __dmul_rn(st, v1));
+}
+
+// Ordered selection with the reference's strict comparisons: `cand` comes
+// later in the sequence than `cur`, so it wins only when strictly better
+// (first element wins ties, _kernels.pyx:195-197, 238-239, 247-248).
+__device__ __forceinline__ bool later_wins(bool late_max, double cur, double cand)
+{
+    return late_max ? (cand > cur) : (cand < cur);
+}
+
+}  // namespace ws

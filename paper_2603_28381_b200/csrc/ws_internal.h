@@ -1,0 +1,128 @@
+// Host-side internals shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ws_common.cuh"
+#include "../../include/warpstar.h"
+
+namespace ws {
+
+struct Error : std::runtime_error {
+    int code;
+    int64_t pin;
+    Error(int c, const std::string& m, int64_t p = -1) : std::runtime_error(m), code(c), pin(p) {}
+};
+
+#define WS_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            if (_e == cudaErrorMemoryAllocation)                                          \
+                throw ::ws::Error(WS_ERR_NOMEM, std::string("cuda: out of device memory at ") + #call); \
+            throw ::ws::Error(WS_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(_e) + \
+                                                " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+        }                                                                                 \
+    } while (0)
+
+#define WS_CHECK_LAUNCH() WS_CUDA(cudaGetLastError())
+
+// Tracked device allocations (freed with the context).
+struct Arena {
+    std::vector<void*> ptrs;
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        WS_CUDA(cudaMalloc(&p, n * sizeof(T)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+};
+
+// Reusable scratch (CUB temp storage etc.).
+struct Scratch {
+    void* p = nullptr;
+    size_t n = 0;
+    void* get(size_t want) {
+        if (want > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            WS_CUDA(cudaMalloc(&p, want));
+            n = want;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// numpy pairwise-sum tree over the 2E endpoint terms (ws_sta.cu)
+struct SumPlan {
+    int n = 0, n_leaves = 0, n_inner = 0;
+    int *leaf_off = nullptr, *leaf_len = nullptr;     // device
+    int *in_left = nullptr, *in_right = nullptr;      // device, children node ids
+    std::vector<int> height_ptr;                      // inner nodes grouped by height
+    int* d_height_ptr = nullptr;
+    int max_height = 0;
+};
+
+struct CornerSlot {
+    Corner d;                  // device pointers
+    bool has_lse = false;      // LSE forward done since the last hard pass
+};
+
+struct Context {
+    Topo t{};
+    Arena topo_mem;
+    Arena val_mem;
+    Scratch scratch;
+    std::vector<CornerSlot> corners;
+    Corner* d_corners = nullptr;      // device copy of every corner's pointers
+    double clock_period = 0.0;
+    int lut_t_len = 0, lut_s_len = 0, lut_l_len = 0;
+    std::vector<int> lv_ptr_host;     // L+1
+    std::vector<int> lv_maxm_host;    // per level: max member count
+    std::vector<int> lv_tree_host;    // per level: any tree net
+    cudaStream_t s_main = nullptr, s_grad = nullptr;
+    std::vector<cudaEvent_t> events;
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_g1 = nullptr;
+    float last_ms_sta = 0.f, last_ms_total = 0.f;
+    SumPlan* tns_plan = nullptr;      // over 2E slack terms
+    int launches_last_run = 0;
+    // CUDA graph cache: key -> exec
+    struct GraphEntry { unsigned key; int c0, nc; double gamma; int loss; int gran; cudaGraphExec_t exec; };
+    std::vector<GraphEntry> graphs;
+    std::vector<int> graph_launches;  // kernels per captured graph
+};
+
+void build_topology(Context& ctx, const ws_design_desc* d);
+void alloc_corner(Context& ctx, CornerSlot& cs);
+void upload_values(Context& ctx, int corner, const ws_design_desc* d);
+void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int loss_kind,
+              int granularity, cudaStream_t s, cudaStream_t g, int w, const Corner* dcs);
+void lse_seed(Context& ctx, int c0, int nc, cudaStream_t s, const Corner* dcs);
+// level-list launches for the legacy per-level shims
+void launch_rc_list(const Topo& t, const Corner* dcs, const int* list, int n, int w, cudaStream_t s);
+void launch_fwd_list(const Topo& t, const Corner* dcs, int n, int lut_s_len, int lut_l_len,
+                     int lut_t_len, cudaStream_t s);
+void launch_bwd_list(const Topo& t, const Corner* dcs, int n, cudaStream_t s);
+void launch_perturb(const Context& ctx, int dst, int src, unsigned long long seed, double sigma,
+                    cudaStream_t s);
+void summary_plan_init(Context& ctx);
+void summary_plan_free(Context& ctx);
+void topo_field_to_host(Context& ctx, int field, int64_t* dst);
+int64_t topo_field_len(Context& ctx, int field);
+
+}  // namespace ws
