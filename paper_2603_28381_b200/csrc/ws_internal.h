@@ -37,7 +37,7 @@ struct Arena {
     template <class T>
     T* alloc(size_t n) {
         void* p = nullptr;
-        if (n == 0) n = 1;
+        if (n < 16) n = 16;   // empty designs still get valid (tiny) buffers
         WS_CUDA(cudaMalloc(&p, n * sizeof(T)));
         ptrs.push_back(p);
         return static_cast<T*>(p);
