@@ -185,6 +185,113 @@ __global__ void k_csr(int N, const int* net_ptr, const int* net_root, const int*
     for (int f = net_ptr[n]; f < net_ptr[n + 1]; f++) pin_list[base + 1 + f - net_ptr[n]] = mem_pin[f];
 }
 
+
+// ---- level-major task layout ------------------------------------------------
+
+__global__ void k_tq(int N, const int* lv_nets, const int* net_root, const int* root_kind,
+                     const int* member_of_pin, const int* net_tree, const int* pin_ep_ptr,
+                     const int* pin_pi, const int* net_ptr, const int* net_a, const int* net_m,
+                     int* tq_root, int* tq_flags, int* tq_f0, int* acnt, int* mcnt)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= N) return;
+    const int n = lv_nets[q], r = net_root[n];
+    int fl = root_kind[n] & TQ_KIND;
+    if (member_of_pin[r] >= 0) fl |= TQ_ROOT_MEMBER;
+    if (net_tree[n]) fl |= TQ_TREE;
+    if (pin_ep_ptr[r + 1] > pin_ep_ptr[r]) fl |= TQ_ROOT_EP;
+    if (pin_pi[r] >= 0) fl |= TQ_ROOT_PI;
+    tq_root[q] = r;
+    tq_flags[q] = fl;
+    tq_f0[q] = net_ptr[n];
+    acnt[q] = (root_kind[n] == ROOT_ARC) ? net_a[n] : 0;
+    mcnt[q] = net_m[n];
+}
+
+__global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* net_in_ptr,
+                     const int* net_in_arc, const int* arc_from, const int* arc_dlut,
+                     const int* arc_slut, int* ta_arc, int* ta_from, ushort4* ta_lut)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= N) return;
+    const int n = lv_nets[q];
+    const int cnt = tq_aptr[q + 1] - tq_aptr[q];
+    for (int k = 0; k < cnt; k++) {
+        const int t = tq_aptr[q] + k, a = net_in_arc[net_in_ptr[n] + k];
+        ta_arc[t] = a;
+        ta_from[t] = arc_from[a];
+        const int* d = arc_dlut + 4 * (size_t)a;
+        const int* s = arc_slut + 4 * (size_t)a;
+        ta_lut[2 * (size_t)t] = make_ushort4(d[0], d[1], d[2], d[3]);
+        ta_lut[2 * (size_t)t + 1] = make_ushort4(s[0], s[1], s[2], s[3]);
+    }
+}
+
+__global__ void k_tm(int N, const int* lv_nets, const int* tq_mptr, const int* net_ptr,
+                     const int* mem_pin, const int* root_net_of_pin, const int* pin_ep_ptr,
+                     const int* mem_out_ptr, int* tm_pin, int* tm_flags, int* ocnt)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= N) return;
+    const int n = lv_nets[q];
+    const int cnt = tq_mptr[q + 1] - tq_mptr[q];
+    for (int k = 0; k < cnt; k++) {
+        const int u = tq_mptr[q] + k, f = net_ptr[n] + k, pin = mem_pin[f];
+        tm_pin[u] = pin;
+        int fl = 0;
+        if (root_net_of_pin[pin] >= 0) fl |= TM_ROOT;
+        if (pin_ep_ptr[pin + 1] > pin_ep_ptr[pin]) fl |= TM_EP;
+        tm_flags[u] = fl;
+        ocnt[u] = mem_out_ptr[f + 1] - mem_out_ptr[f];
+    }
+}
+
+__global__ void k_to(int N, const int* lv_nets, const int* tq_mptr, const int* net_ptr,
+                     const int* tm_optr, const int* mem_out_ptr, const int* mem_out_arc,
+                     const int* arc_to, int* to_arc, int* to_to)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= N) return;
+    const int n = lv_nets[q];
+    const int cnt = tq_mptr[q + 1] - tq_mptr[q];
+    for (int k = 0; k < cnt; k++) {
+        const int u = tq_mptr[q] + k, f = net_ptr[n] + k;
+        for (int o = mem_out_ptr[f]; o < mem_out_ptr[f + 1]; o++) {
+            const int v = tm_optr[u] + (o - mem_out_ptr[f]);
+            const int a = mem_out_arc[o];
+            to_arc[v] = a;
+            to_to[v] = arc_to[a];
+        }
+    }
+}
+
+__global__ void k_blk_local(int nb, const int* blk_q0, const int* tq_mptr, int* tq_flags,
+                            int* tm_flags)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int q0 = blk_q0[b], q1 = blk_q0[b + 1];
+    if (q1 - q0 == 1 && tq_mptr[q1] - tq_mptr[q0] > BIG_M) tq_flags[q0] |= TQ_BIG;
+    for (int q = q0; q < q1; q++)
+        for (int u = tq_mptr[q]; u < tq_mptr[q + 1]; u++) tm_flags[u] |= (q - q0) << 8;
+}
+
+__global__ void k_fin_flags(int P, const int* member_of_pin, const int* root_net_of_pin,
+                            const int* pin_out_ptr, uint8_t* flag)
+{
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const bool nonmem = member_of_pin[p] < 0;
+    const bool root = root_net_of_pin[p] >= 0;
+    flag[p] = nonmem && (!root || pin_out_ptr[p + 1] > pin_out_ptr[p]);
+}
+
+__global__ void k_fin_kind(int n, const int* fin_pins, const int* root_net_of_pin, int* fin_flags)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) fin_flags[i] = root_net_of_pin[fin_pins[i]] >= 0 ? 1 : 0;
+}
+
 int bits_for(int maxkey)
 {
     int b = 1;
@@ -259,6 +366,123 @@ int reduce_max(Scratch& sc, Arena& ar, const int* a, int n, cudaStream_t s)
 }
 
 }  // namespace
+
+
+// Level-major task arrays and the thread-block partition of every level.
+void build_tasks(Context& ctx)
+{
+    Topo& t = ctx.t;
+    Arena& ar = ctx.topo_mem;
+    Scratch& sc = ctx.scratch;
+    cudaStream_t s = ctx.s_main;
+    const int N = t.N, M = t.M, P = t.P;
+    if (t.NL > 65535) throw Error(WS_ERR_VALUE, "more than 65535 LUTs in the pool");
+    t.tq_root = ar.alloc<int>(N);
+    t.tq_flags = ar.alloc<int>(N);
+    t.tq_f0 = ar.alloc<int>(N);
+    t.tq_aptr = ar.alloc<int>(N + 1);
+    t.tq_mptr = ar.alloc<int>(N + 1);
+    int* acnt = ar.alloc<int>(N + 1);
+    int* mcnt = ar.alloc<int>(N + 1);
+    WS_CUDA(cudaMemsetAsync(acnt, 0, sizeof(int) * (size_t)(N + 1), s));
+    WS_CUDA(cudaMemsetAsync(mcnt, 0, sizeof(int) * (size_t)(N + 1), s));
+    if (N) {
+        k_tq<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.net_root, t.root_kind, t.member_of_pin,
+                                           t.net_tree, t.pin_ep_ptr, t.pin_pi, t.net_ptr, t.net_a,
+                                           t.net_m, t.tq_root, t.tq_flags, t.tq_f0, acnt, mcnt);
+        WS_CHECK_LAUNCH();
+    }
+    auto scan = [&](int* in, int* out, int n) {
+        size_t bytes = 0;
+        WS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n + 1, s));
+        void* tmp = sc.get(bytes);
+        WS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n + 1, s));
+    };
+    scan(acnt, t.tq_aptr, N);
+    scan(mcnt, t.tq_mptr, N);
+    int na = 0;
+    WS_CUDA(cudaMemcpyAsync(&na, t.tq_aptr + N, sizeof(int), cudaMemcpyDeviceToHost, s));
+    WS_CUDA(cudaStreamSynchronize(s));
+    t.ta_arc = ar.alloc<int>(na);
+    t.ta_from = ar.alloc<int>(na);
+    t.ta_lut = ar.alloc<ushort4>(2 * (size_t)na);
+    t.tm_pin = ar.alloc<int>(M);
+    t.tm_flags = ar.alloc<int>(M);
+    t.tm_optr = ar.alloc<int>(M + 1);
+    int* ocnt = ar.alloc<int>(M + 1);
+    WS_CUDA(cudaMemsetAsync(ocnt, 0, sizeof(int) * (size_t)(M + 1), s));
+    if (N) {
+        k_ta<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_aptr, t.net_in_ptr, t.net_in_arc,
+                                           t.arc_from, t.arc_dlut, t.arc_slut, t.ta_arc, t.ta_from,
+                                           t.ta_lut);
+        k_tm<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_mptr, t.net_ptr, t.mem_pin,
+                                           t.root_net_of_pin, t.pin_ep_ptr, t.mem_out_ptr, t.tm_pin,
+                                           t.tm_flags, ocnt);
+        WS_CHECK_LAUNCH();
+    }
+    scan(ocnt, t.tm_optr, M);
+    int no = 0;
+    WS_CUDA(cudaMemcpyAsync(&no, t.tm_optr + M, sizeof(int), cudaMemcpyDeviceToHost, s));
+    WS_CUDA(cudaStreamSynchronize(s));
+    t.to_arc = ar.alloc<int>(no);
+    t.to_to = ar.alloc<int>(no);
+    if (N) {
+        k_to<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_mptr, t.net_ptr, t.tm_optr,
+                                           t.mem_out_ptr, t.mem_out_arc, t.arc_to, t.to_arc, t.to_to);
+        WS_CHECK_LAUNCH();
+    }
+    // thread-block partition, level by level: big nets alone, others packed
+    // up to BLK_Q nets / BLK_M members
+    std::vector<int> mptr(N + 1);
+    WS_CUDA(cudaMemcpy(mptr.data(), t.tq_mptr, sizeof(int) * (size_t)(N + 1), cudaMemcpyDeviceToHost));
+    std::vector<int> q0s;
+    ctx.lvb_ptr_host.assign(t.L + 1, 0);
+    for (int li = 0; li < t.L; li++) {
+        ctx.lvb_ptr_host[li] = (int)q0s.size();
+        int q = ctx.lv_ptr_host[li], qe = ctx.lv_ptr_host[li + 1];
+        int cur_q = -1, cur_n = 0, cur_m = 0;
+        for (; q < qe; q++) {
+            const int m = mptr[q + 1] - mptr[q];
+            if (m > BIG_M) {
+                q0s.push_back(q);
+                cur_q = -1;
+                continue;
+            }
+            if (cur_q < 0 || cur_n >= BLK_Q || cur_m + m > BLK_M) {
+                q0s.push_back(q);
+                cur_q = q;
+                cur_n = 0;
+                cur_m = 0;
+            }
+            cur_n++;
+            cur_m += m;
+        }
+    }
+    ctx.lvb_ptr_host[t.L] = (int)q0s.size();
+    t.n_blocks = (int)q0s.size();
+    q0s.push_back(N);
+    t.blk_q0 = ar.alloc<int>(q0s.size());
+    WS_CUDA(cudaMemcpy(t.blk_q0, q0s.data(), sizeof(int) * q0s.size(), cudaMemcpyHostToDevice));
+    if (t.n_blocks) {
+        k_blk_local<<<blocks_for(t.n_blocks), TPB, 0, s>>>(t.n_blocks, t.blk_q0, t.tq_mptr,
+                                                           t.tq_flags, t.tm_flags);
+        WS_CHECK_LAUNCH();
+    }
+    // pins finished after the level loop
+    uint8_t* ff = ar.alloc<uint8_t>(P);
+    if (P) {
+        k_fin_flags<<<blocks_for(P), TPB, 0, s>>>(P, t.member_of_pin, t.root_net_of_pin,
+                                                  t.pin_out_ptr, ff);
+        WS_CHECK_LAUNCH();
+    }
+    t.n_fin = P ? select_flagged(sc, ar, ff, P, &t.fin_pins, s) : 0;
+    t.fin_flags = ar.alloc<int>(t.n_fin);
+    if (t.n_fin) {
+        k_fin_kind<<<blocks_for(t.n_fin), TPB, 0, s>>>(t.n_fin, t.fin_pins, t.root_net_of_pin,
+                                                       t.fin_flags);
+        WS_CHECK_LAUNCH();
+    }
+}
 
 void build_topology(Context& ctx, const ws_design_desc* d)
 {
@@ -502,6 +726,8 @@ void build_topology(Context& ctx, const ws_design_desc* d)
                 ctx.lv_tree_host[li] |= tr[lvn[q]];
             }
     }
+
+    build_tasks(ctx);
     WS_CUDA(cudaStreamSynchronize(s));
 }
 

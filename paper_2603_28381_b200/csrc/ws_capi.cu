@@ -144,6 +144,8 @@ void alloc_corner(Context& ctx, CornerSlot& cs)
     const int nl = ctx.tns_plan ? std::max(1, ctx.tns_plan->n_leaves) : 1;
     d.red_tmp = ar.alloc<double>(3 * (size_t)(2 * nl));
     d.summary = ar.alloc<double>(4);
+    d.sync_ctr = ar.alloc<unsigned>(4);
+    WS_CUDA(cudaMemset(d.sync_ctr, 0, 4 * sizeof(unsigned)));
     // arrays that are not fully rewritten by every pass start defined
     WS_CUDA(cudaMemset(d.arc_delay, 0, sizeof(double) * 4 * (size_t)std::max(t.A, 1)));
     WS_CUDA(cudaMemset(d.weights, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));
@@ -209,9 +211,7 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
         for (auto& cs : c.corners) ws::alloc_corner(c, cs);
         for (int k = 0; k < n_corners; k++) ws::upload_values(c, k, d);
         c.d_corners = c.topo_mem.alloc<ws::Corner>(n_corners);
-        int any_tree = 0;
-        for (int v : c.lv_tree_host) any_tree |= v;
-        if (any_tree) ws::ensure_tree_scratch(c);
+        ws::ensure_tree_scratch(c);   // tree-net RC and big-net fold scratch
         std::vector<ws::Corner> v;
         for (auto& cs : c.corners) v.push_back(cs.d);
         WS_CUDA(cudaMemcpy(c.d_corners, v.data(), sizeof(ws::Corner) * v.size(), cudaMemcpyHostToDevice));
@@ -326,7 +326,6 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
         if (reduce_width < 1 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
             throw ws::Error(WS_ERR_VALUE, "reduce_width must be a power of two in [1, 32]");
         if (granularity < 1) throw ws::Error(WS_ERR_VALUE, "granularity must be >= 1");
-        if (reduce_width != 8) ws::ensure_tree_scratch(c);
         cudaStream_t s = as_stream(stream, c.s_main);
         cudaStream_t g = as_stream(stream_grad, c.s_grad);
         if (flags & WS_RUN_GRAPH) {
@@ -342,7 +341,7 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
                 WS_CUDA(cudaStreamCreateWithFlags(&capg, cudaStreamNonBlocking));
                 WS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
                 ws::run_pass(c, corner0, n_corners, key, gamma, loss_kind, granularity, cap, capg,
-                             reduce_width, c.d_corners);
+                             reduce_width);
                 cudaGraph_t graph;
                 WS_CUDA(cudaStreamEndCapture(cap, &graph));
                 WS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -360,7 +359,7 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
             c.launches_last_run = cnt;
         } else {
             ws::run_pass(c, corner0, n_corners, flags, gamma, loss_kind, granularity, s, g,
-                         reduce_width, c.d_corners);
+                         reduce_width);
         }
         if (flags & WS_RUN_HARD)
             for (int k = 0; k < n_corners; k++) c.corners[corner0 + k].has_lse = false;

@@ -38,7 +38,40 @@ struct Topo {
     int *free_pins;                  // pins that belong to no net (n_free)
     int *nonmem_src;                 // non-member pins that source arcs
     int n_nonmem_src;
+
+    // ---- level-major task layout (ws_build.cu: build_tasks) --------------
+    // q = position in lv_nets (nets level by level, ascending id per level).
+    // Everything a level kernel needs about net q, its in-arcs and its
+    // members is stored contiguously in q order so one coalesced load per
+    // array replaces the reference's pointer chasing.
+    int *tq_root;      // [N] root pin
+    int *tq_flags;     // [N] TQ_* bits
+    int *tq_f0;        // [N] first member index (original member order)
+    int *tq_aptr;      // [N+1] in-arcs of q: ta_*[tq_aptr[q] .. tq_aptr[q+1])
+    int *tq_mptr;      // [N+1] members of q: tm_*[tq_mptr[q] .. tq_mptr[q+1])
+    int *ta_arc;       // [A'] original arc id
+    int *ta_from;      // [A'] arc source pin
+    ushort4 *ta_lut;   // [2*A'] delay LUT ids (ER EF LR LF), then slew LUT ids
+    int *tm_pin;       // [M] member pin
+    int *tm_flags;     // [M] TM_* bits | (net index within its block) << 8
+    int *tm_optr;      // [M+1] out-arcs of member slot u: to_*[tm_optr[u] .. )
+    int *to_arc;       // [A''] original arc id
+    int *to_to;        // [A''] arc target pin
+    int *blk_q0;       // [n_blocks+1] first q of each thread block
+    int n_blocks;
+    int *fin_pins;     // pins finished after the level loop (free pins, PI roots with out-arcs)
+    int *fin_flags;    // 1 = accumulate onto the level-loop adjoint (root), 0 = fresh
+    int n_fin;
 };
+
+// tq_flags
+constexpr int TQ_KIND = 3, TQ_ROOT_MEMBER = 4, TQ_TREE = 8, TQ_ROOT_EP = 16, TQ_ROOT_PI = 32,
+              TQ_BIG = 64;
+// tm_flags
+constexpr int TM_ROOT = 1, TM_EP = 2;
+// block partition: a "big" net (more than BIG_M members) gets a block of its
+// own; other blocks hold <= BLK_Q nets and <= BLK_M members
+constexpr int BIG_M = 32, BLK_Q = 64, BLK_M = 256, PASS_TPB = 256;
 
 // Values and state of one corner.  (P,4) arrays are row-major 32-byte
 // records, exactly the reference's TimingState layout (sta.py:41-48).
@@ -50,9 +83,10 @@ struct Corner {
     // GradientState (late cols only; diff.py:61-72)
     double *lse_at, *weights, *d_arc, *d_edge, *adjoint;
     // scratch for tree nets (RC fold) and the summary reductions
-    double *mem_buf, *mem_dbuf;
+    double *mem_buf, *mem_dbuf;      // [M*4] each: RC tree fold / big-net fold scratch
     double *red_tmp;   // pairwise-sum node values
     double *summary;   // [tns, wns, loss]
+    unsigned *sync_ctr;  // last-block-done counter of the summary kernel
 };
 
 struct LutView {
@@ -107,6 +141,52 @@ __device__ __forceinline__ double lut_interp(const LutView& L, int lut, double q
 __device__ __forceinline__ bool later_wins(bool late_max, double cur, double cand)
 {
     return late_max ? (cand > cur) : (cand < cur);
+}
+
+// ---------------------------------------------------------------------------
+// LUT pool staging into shared memory (north_star item 3)
+
+struct LutSrc {
+    const int *s_ptr, *l_ptr, *t_ptr;
+    const double *s, *l;
+    int nl, s_len, l_len, t_len;
+};
+
+__host__ __device__ inline size_t lut_smem_bytes(int nl, int s_len, int l_len, int t_len)
+{
+    size_t ints = 3 * (size_t)(nl + 1);
+    ints = (ints + 1) & ~(size_t)1;
+    return ints * 4 + (size_t)(s_len + l_len + t_len) * 8;
+}
+
+// Copies the pool (axes + this corner's tables) into smem when it fits
+// (use_smem), else views global memory.  Contains __syncthreads.
+__device__ __forceinline__ LutView stage_luts(const LutSrc& src, const double* t_flat,
+                                              bool use_smem, unsigned char* smem)
+{
+    LutView v;
+    if (!use_smem) {
+        v.s_ptr = src.s_ptr; v.l_ptr = src.l_ptr; v.t_ptr = src.t_ptr;
+        v.s = src.s; v.l = src.l; v.t = t_flat;
+        return v;
+    }
+    const int n1 = src.nl + 1;
+    int* ip = reinterpret_cast<int*>(smem);
+    size_t ints = 3 * (size_t)n1;
+    ints = (ints + 1) & ~(size_t)1;
+    double* dp = reinterpret_cast<double*>(smem + ints * 4);
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+        ip[i] = src.s_ptr[i];
+        ip[n1 + i] = src.l_ptr[i];
+        ip[2 * n1 + i] = src.t_ptr[i];
+    }
+    for (int i = threadIdx.x; i < src.s_len; i += blockDim.x) dp[i] = src.s[i];
+    for (int i = threadIdx.x; i < src.l_len; i += blockDim.x) dp[src.s_len + i] = src.l[i];
+    for (int i = threadIdx.x; i < src.t_len; i += blockDim.x) dp[src.s_len + src.l_len + i] = t_flat[i];
+    __syncthreads();
+    v.s_ptr = ip; v.l_ptr = ip + n1; v.t_ptr = ip + 2 * n1;
+    v.s = dp; v.l = dp + src.s_len; v.t = dp + src.s_len + src.l_len;
+    return v;
 }
 
 }  // namespace ws

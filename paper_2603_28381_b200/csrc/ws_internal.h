@@ -95,6 +95,7 @@ struct Context {
     std::vector<int> lv_ptr_host;     // L+1
     std::vector<int> lv_maxm_host;    // per level: max member count
     std::vector<int> lv_tree_host;    // per level: any tree net
+    std::vector<int> lvb_ptr_host;    // per level: first thread block (L+1)
     cudaStream_t s_main = nullptr, s_grad = nullptr;
     std::vector<cudaEvent_t> events;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_g1 = nullptr;
@@ -111,8 +112,7 @@ void build_topology(Context& ctx, const ws_design_desc* d);
 void alloc_corner(Context& ctx, CornerSlot& cs);
 void upload_values(Context& ctx, int corner, const ws_design_desc* d);
 void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int loss_kind,
-              int granularity, cudaStream_t s, cudaStream_t g, int w, const Corner* dcs);
-void lse_seed(Context& ctx, int c0, int nc, cudaStream_t s, const Corner* dcs);
+              int granularity, cudaStream_t s, cudaStream_t g, int w);
 // level-list launches for the legacy per-level shims
 void launch_rc_list(const Topo& t, const Corner* dcs, const int* list, int n, int w, cudaStream_t s);
 void launch_fwd_list(const Topo& t, const Corner* dcs, int n, int lut_s_len, int lut_l_len,
