@@ -190,8 +190,9 @@ __global__ void k_csr(int N, const int* net_ptr, const int* net_root, const int*
 
 __global__ void k_tq(int N, const int* lv_nets, const int* net_root, const int* root_kind,
                      const int* member_of_pin, const int* net_tree, const int* pin_ep_ptr,
-                     const int* pin_pi, const int* net_ptr, const int* net_a, const int* net_m,
-                     int* tq_root, int* tq_flags, int* tq_f0, int* acnt, int* mcnt)
+                     const int* pin_ep_idx, const int* pin_pi, const int* net_ptr,
+                     const int* net_a, const int* net_m, int* tq_root, int* tq_flags, int* tq_f0,
+                     int* tq_e1, int* acnt, int* mcnt)
 {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N) return;
@@ -199,18 +200,22 @@ __global__ void k_tq(int N, const int* lv_nets, const int* net_root, const int* 
     int fl = root_kind[n] & TQ_KIND;
     if (member_of_pin[r] >= 0) fl |= TQ_ROOT_MEMBER;
     if (net_tree[n]) fl |= TQ_TREE;
-    if (pin_ep_ptr[r + 1] > pin_ep_ptr[r]) fl |= TQ_ROOT_EP;
+    const int ne = pin_ep_ptr[r + 1] - pin_ep_ptr[r];
+    if (ne > 0) fl |= TQ_ROOT_EP;
+    if (ne > 1) fl |= TQ_MULTI_EP;
     if (pin_pi[r] >= 0) fl |= TQ_ROOT_PI;
     tq_root[q] = r;
     tq_flags[q] = fl;
     tq_f0[q] = net_ptr[n];
+    tq_e1[q] = ne > 0 ? pin_ep_idx[pin_ep_ptr[r]] : -1;
     acnt[q] = (root_kind[n] == ROOT_ARC) ? net_a[n] : 0;
     mcnt[q] = net_m[n];
 }
 
-__global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* net_in_ptr,
-                     const int* net_in_arc, const int* arc_from, const int* arc_dlut,
-                     const int* arc_slut, int* ta_arc, int* ta_from, ushort4* ta_lut)
+__global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* tq_root,
+                     const int* net_in_ptr, const int* net_in_arc, const int* arc_from,
+                     const int* arc_dlut, const int* arc_slut, int* ta_arc, int* ta_from,
+                     int* ta_root, ushort4* ta_lut)
 {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N) return;
@@ -220,16 +225,19 @@ __global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* n
         const int t = tq_aptr[q] + k, a = net_in_arc[net_in_ptr[n] + k];
         ta_arc[t] = a;
         ta_from[t] = arc_from[a];
+        ta_root[t] = tq_root[q];
         const int* d = arc_dlut + 4 * (size_t)a;
-        const int* s = arc_slut + 4 * (size_t)a;
+        const int* sl = arc_slut + 4 * (size_t)a;
         ta_lut[2 * (size_t)t] = make_ushort4(d[0], d[1], d[2], d[3]);
-        ta_lut[2 * (size_t)t + 1] = make_ushort4(s[0], s[1], s[2], s[3]);
+        ta_lut[2 * (size_t)t + 1] = make_ushort4(sl[0], sl[1], sl[2], sl[3]);
     }
 }
 
 __global__ void k_tm(int N, const int* lv_nets, const int* tq_mptr, const int* net_ptr,
                      const int* mem_pin, const int* root_net_of_pin, const int* pin_ep_ptr,
-                     const int* mem_out_ptr, int* tm_pin, int* tm_flags, int* ocnt)
+                     const int* pin_ep_idx, const int* mem_out_ptr, const int* mem_out_arc,
+                     const int* arc_to, int* tm_pin, int* tm_flags, int* tm_o1_to,
+                     int* tm_o1_arc, int* tm_e1, int* ocnt)
 {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N) return;
@@ -240,9 +248,15 @@ __global__ void k_tm(int N, const int* lv_nets, const int* tq_mptr, const int* n
         tm_pin[u] = pin;
         int fl = 0;
         if (root_net_of_pin[pin] >= 0) fl |= TM_ROOT;
-        if (pin_ep_ptr[pin + 1] > pin_ep_ptr[pin]) fl |= TM_EP;
+        const int ne = pin_ep_ptr[pin + 1] - pin_ep_ptr[pin];
+        if (ne > 0) fl |= TM_EP;
+        if (ne > 1) fl |= TM_MULTI_EP;
         tm_flags[u] = fl;
-        ocnt[u] = mem_out_ptr[f + 1] - mem_out_ptr[f];
+        tm_e1[u] = ne > 0 ? pin_ep_idx[pin_ep_ptr[pin]] : -1;
+        const int o0 = mem_out_ptr[f], o1 = mem_out_ptr[f + 1];
+        ocnt[u] = o1 - o0;
+        tm_o1_arc[u] = o1 > o0 ? mem_out_arc[o0] : -1;
+        tm_o1_to[u] = o1 > o0 ? arc_to[mem_out_arc[o0]] : -1;
     }
 }
 
@@ -265,15 +279,19 @@ __global__ void k_to(int N, const int* lv_nets, const int* tq_mptr, const int* n
     }
 }
 
-__global__ void k_blk_local(int nb, const int* blk_q0, const int* tq_mptr, int* tq_flags,
-                            int* tm_flags)
+// task-local net index of every arc and member
+__global__ void k_task_local(int T, const int4* tk_a, const int4* tk_b, const int* tq_aptr,
+                             const int* tq_mptr, int* ta_q, int* tm_flags)
 {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    const int q0 = blk_q0[b], q1 = blk_q0[b + 1];
-    if (q1 - q0 == 1 && tq_mptr[q1] - tq_mptr[q0] > BIG_M) tq_flags[q0] |= TQ_BIG;
-    for (int q = q0; q < q1; q++)
-        for (int u = tq_mptr[q]; u < tq_mptr[q + 1]; u++) tm_flags[u] |= (q - q0) << 8;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= T) return;
+    const int4 a = tk_a[k], b = tk_b[k];
+    for (int qi = 0; qi < a.y; qi++) {
+        const int q = a.x + qi;
+        for (int t = tq_aptr[q]; t < tq_aptr[q + 1]; t++) ta_q[t] = qi;
+        const int u0 = max(tq_mptr[q], b.x), u1 = min(tq_mptr[q + 1], b.x + b.y);
+        for (int u = u0; u < u1; u++) tm_flags[u] = (tm_flags[u] & 0xff) | (qi << 8);
+    }
 }
 
 __global__ void k_fin_flags(int P, const int* member_of_pin, const int* root_net_of_pin,
@@ -368,7 +386,7 @@ int reduce_max(Scratch& sc, Arena& ar, const int* a, int n, cudaStream_t s)
 }  // namespace
 
 
-// Level-major task arrays and the thread-block partition of every level.
+// Level-major task arrays and the task partition of every level.
 void build_tasks(Context& ctx)
 {
     Topo& t = ctx.t;
@@ -380,6 +398,7 @@ void build_tasks(Context& ctx)
     t.tq_root = ar.alloc<int>(N);
     t.tq_flags = ar.alloc<int>(N);
     t.tq_f0 = ar.alloc<int>(N);
+    t.tq_e1 = ar.alloc<int>(N);
     t.tq_aptr = ar.alloc<int>(N + 1);
     t.tq_mptr = ar.alloc<int>(N + 1);
     int* acnt = ar.alloc<int>(N + 1);
@@ -388,8 +407,9 @@ void build_tasks(Context& ctx)
     WS_CUDA(cudaMemsetAsync(mcnt, 0, sizeof(int) * (size_t)(N + 1), s));
     if (N) {
         k_tq<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.net_root, t.root_kind, t.member_of_pin,
-                                           t.net_tree, t.pin_ep_ptr, t.pin_pi, t.net_ptr, t.net_a,
-                                           t.net_m, t.tq_root, t.tq_flags, t.tq_f0, acnt, mcnt);
+                                           t.net_tree, t.pin_ep_ptr, t.pin_ep_idx, t.pin_pi,
+                                           t.net_ptr, t.net_a, t.net_m, t.tq_root, t.tq_flags,
+                                           t.tq_f0, t.tq_e1, acnt, mcnt);
         WS_CHECK_LAUNCH();
     }
     auto scan = [&](int* in, int* out, int n) {
@@ -405,19 +425,25 @@ void build_tasks(Context& ctx)
     WS_CUDA(cudaStreamSynchronize(s));
     t.ta_arc = ar.alloc<int>(na);
     t.ta_from = ar.alloc<int>(na);
+    t.ta_root = ar.alloc<int>(na);
+    t.ta_q = ar.alloc<int>(na);
     t.ta_lut = ar.alloc<ushort4>(2 * (size_t)na);
     t.tm_pin = ar.alloc<int>(M);
     t.tm_flags = ar.alloc<int>(M);
     t.tm_optr = ar.alloc<int>(M + 1);
+    t.tm_o1_to = ar.alloc<int>(M);
+    t.tm_o1_arc = ar.alloc<int>(M);
+    t.tm_e1 = ar.alloc<int>(M);
     int* ocnt = ar.alloc<int>(M + 1);
     WS_CUDA(cudaMemsetAsync(ocnt, 0, sizeof(int) * (size_t)(M + 1), s));
     if (N) {
-        k_ta<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_aptr, t.net_in_ptr, t.net_in_arc,
-                                           t.arc_from, t.arc_dlut, t.arc_slut, t.ta_arc, t.ta_from,
-                                           t.ta_lut);
+        k_ta<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_aptr, t.tq_root, t.net_in_ptr,
+                                           t.net_in_arc, t.arc_from, t.arc_dlut, t.arc_slut,
+                                           t.ta_arc, t.ta_from, t.ta_root, t.ta_lut);
         k_tm<<<blocks_for(N), TPB, 0, s>>>(N, t.lv_nets, t.tq_mptr, t.net_ptr, t.mem_pin,
-                                           t.root_net_of_pin, t.pin_ep_ptr, t.mem_out_ptr, t.tm_pin,
-                                           t.tm_flags, ocnt);
+                                           t.root_net_of_pin, t.pin_ep_ptr, t.pin_ep_idx,
+                                           t.mem_out_ptr, t.mem_out_arc, t.arc_to, t.tm_pin,
+                                           t.tm_flags, t.tm_o1_to, t.tm_o1_arc, t.tm_e1, ocnt);
         WS_CHECK_LAUNCH();
     }
     scan(ocnt, t.tm_optr, M);
@@ -431,41 +457,79 @@ void build_tasks(Context& ctx)
                                            t.mem_out_ptr, t.mem_out_arc, t.arc_to, t.to_arc, t.to_to);
         WS_CHECK_LAUNCH();
     }
-    // thread-block partition, level by level: big nets alone, others packed
-    // up to BLK_Q nets / BLK_M members
-    std::vector<int> mptr(N + 1);
+    // ---- task partition, level by level (host; one-time) -------------------
+    std::vector<int> mptr(N + 1), aptr(N + 1), fl(N);
     WS_CUDA(cudaMemcpy(mptr.data(), t.tq_mptr, sizeof(int) * (size_t)(N + 1), cudaMemcpyDeviceToHost));
-    std::vector<int> q0s;
-    ctx.lvb_ptr_host.assign(t.L + 1, 0);
+    WS_CUDA(cudaMemcpy(aptr.data(), t.tq_aptr, sizeof(int) * (size_t)(N + 1), cudaMemcpyDeviceToHost));
+    if (N) WS_CUDA(cudaMemcpy(fl.data(), t.tq_flags, sizeof(int) * (size_t)N, cudaMemcpyDeviceToHost));
+    std::vector<int4> ta_, tb_;
+    std::vector<int> nch, part0;
+    int n_parts = 0;
+    ctx.lvt_ptr_host.assign(t.L + 1, 0);
     for (int li = 0; li < t.L; li++) {
-        ctx.lvb_ptr_host[li] = (int)q0s.size();
-        int q = ctx.lv_ptr_host[li], qe = ctx.lv_ptr_host[li + 1];
-        int cur_q = -1, cur_n = 0, cur_m = 0;
-        for (; q < qe; q++) {
-            const int m = mptr[q + 1] - mptr[q];
-            if (m > BIG_M) {
-                q0s.push_back(q);
-                cur_q = -1;
+        ctx.lvt_ptr_host[li] = (int)ta_.size();
+        int cq = -1, cn = 0, ca = 0, cm = 0;
+        auto flush = [&]() {
+            if (cq >= 0) {
+                ta_.push_back(make_int4(cq, cn, aptr[cq], ca));
+                tb_.push_back(make_int4(mptr[cq], cm, 0, -1));
+            }
+            cq = -1; cn = ca = cm = 0;
+        };
+        for (int q = ctx.lv_ptr_host[li]; q < ctx.lv_ptr_host[li + 1]; q++) {
+            const int m = mptr[q + 1] - mptr[q], a = aptr[q + 1] - aptr[q];
+            const bool tree = fl[q] & TQ_TREE;
+            if (a > TASK_A || (m > TASK_M && tree)) {
+                flush();
+                int f = 0;
+                if (a > TASK_A) f |= TK_WIDE;
+                if (m > TASK_M) f |= TK_LOOP;
+                ta_.push_back(make_int4(q, 1, aptr[q], a));
+                tb_.push_back(make_int4(mptr[q], m, f, -1));
                 continue;
             }
-            if (cur_q < 0 || cur_n >= BLK_Q || cur_m + m > BLK_M) {
-                q0s.push_back(q);
-                cur_q = q;
-                cur_n = 0;
-                cur_m = 0;
+            if (m > TASK_M) {           // big star net: chunks of TASK_M members
+                flush();
+                const int k = (m + TASK_M - 1) / TASK_M, slot = (int)nch.size();
+                nch.push_back(k);
+                part0.push_back(n_parts);
+                n_parts += k;
+                for (int c = 0; c < k; c++) {
+                    ta_.push_back(make_int4(q, 1, aptr[q], a));
+                    tb_.push_back(make_int4(mptr[q] + c * TASK_M, std::min(TASK_M, m - c * TASK_M),
+                                            TK_CHUNK, slot));
+                }
+                continue;
             }
-            cur_n++;
-            cur_m += m;
+            if (cq < 0 || cn >= TASK_Q || ca + a > TASK_A || cm + m > TASK_M) {
+                flush();
+                cq = q;
+            }
+            cn++;
+            ca += a;
+            cm += m;
         }
+        flush();
     }
-    ctx.lvb_ptr_host[t.L] = (int)q0s.size();
-    t.n_blocks = (int)q0s.size();
-    q0s.push_back(N);
-    t.blk_q0 = ar.alloc<int>(q0s.size());
-    WS_CUDA(cudaMemcpy(t.blk_q0, q0s.data(), sizeof(int) * q0s.size(), cudaMemcpyHostToDevice));
-    if (t.n_blocks) {
-        k_blk_local<<<blocks_for(t.n_blocks), TPB, 0, s>>>(t.n_blocks, t.blk_q0, t.tq_mptr,
-                                                           t.tq_flags, t.tm_flags);
+    ctx.lvt_ptr_host[t.L] = (int)ta_.size();
+    t.n_tasks = (int)ta_.size();
+    t.tk_a = ar.alloc<int4>(ta_.size());
+    t.tk_b = ar.alloc<int4>(tb_.size());
+    if (!ta_.empty()) {
+        WS_CUDA(cudaMemcpy(t.tk_a, ta_.data(), sizeof(int4) * ta_.size(), cudaMemcpyHostToDevice));
+        WS_CUDA(cudaMemcpy(t.tk_b, tb_.data(), sizeof(int4) * tb_.size(), cudaMemcpyHostToDevice));
+    }
+    t.n_big = (int)nch.size();
+    t.n_parts = n_parts;
+    t.bn_nch = ar.alloc<int>(nch.size());
+    t.bn_part0 = ar.alloc<int>(part0.size());
+    if (!nch.empty()) {
+        WS_CUDA(cudaMemcpy(t.bn_nch, nch.data(), sizeof(int) * nch.size(), cudaMemcpyHostToDevice));
+        WS_CUDA(cudaMemcpy(t.bn_part0, part0.data(), sizeof(int) * part0.size(), cudaMemcpyHostToDevice));
+    }
+    if (t.n_tasks) {
+        k_task_local<<<blocks_for(t.n_tasks), TPB, 0, s>>>(t.n_tasks, t.tk_a, t.tk_b, t.tq_aptr,
+                                                           t.tq_mptr, t.ta_q, t.tm_flags);
         WS_CHECK_LAUNCH();
     }
     // pins finished after the level loop

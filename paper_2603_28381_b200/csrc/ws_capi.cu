@@ -146,6 +146,9 @@ void alloc_corner(Context& ctx, CornerSlot& cs)
     d.summary = ar.alloc<double>(4);
     d.sync_ctr = ar.alloc<unsigned>(4);
     WS_CUDA(cudaMemset(d.sync_ctr, 0, 4 * sizeof(unsigned)));
+    d.big_part = ar.alloc<double>(8 * (size_t)std::max(t.n_parts, 1));
+    d.big_ctr = ar.alloc<unsigned>(4 * (size_t)std::max(t.n_big, 1));
+    WS_CUDA(cudaMemset(d.big_ctr, 0, 4 * sizeof(unsigned) * (size_t)std::max(t.n_big, 1)));
     // arrays that are not fully rewritten by every pass start defined
     WS_CUDA(cudaMemset(d.arc_delay, 0, sizeof(double) * 4 * (size_t)std::max(t.A, 1)));
     WS_CUDA(cudaMemset(d.weights, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));

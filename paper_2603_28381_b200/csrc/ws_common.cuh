@@ -49,16 +49,28 @@ struct Topo {
     int *tq_f0;        // [N] first member index (original member order)
     int *tq_aptr;      // [N+1] in-arcs of q: ta_*[tq_aptr[q] .. tq_aptr[q+1])
     int *tq_mptr;      // [N+1] members of q: tm_*[tq_mptr[q] .. tq_mptr[q+1])
+    int *tq_e1;        // [N] first endpoint entry of the root (or -1)
     int *ta_arc;       // [A'] original arc id
     int *ta_from;      // [A'] arc source pin
+    int *ta_root;      // [A'] root pin of the arc's net
+    int *ta_q;         // [A'] index of the arc's net within its task
     ushort4 *ta_lut;   // [2*A'] delay LUT ids (ER EF LR LF), then slew LUT ids
     int *tm_pin;       // [M] member pin
-    int *tm_flags;     // [M] TM_* bits | (net index within its block) << 8
+    int *tm_flags;     // [M] TM_* bits | (net index within its task) << 8
     int *tm_optr;      // [M+1] out-arcs of member slot u: to_*[tm_optr[u] .. )
+    int *tm_o1_to;     // [M] first out-arc's target pin (or -1)
+    int *tm_o1_arc;    // [M] first out-arc id (or -1)
+    int *tm_e1;        // [M] first endpoint entry of the pin (or -1)
     int *to_arc;       // [A''] original arc id
     int *to_to;        // [A''] arc target pin
-    int *blk_q0;       // [n_blocks+1] first q of each thread block
-    int n_blocks;
+    // tasks: a level is a contiguous task range; a task is one thread block's
+    // unit of work: <= TASK_Q nets, <= TASK_A in-arcs, <= TASK_M members
+    int4 *tk_a;        // [T] q0, nq, a0, na
+    int4 *tk_b;        // [T] m0, nm, flags (TK_*), big-net slot (TK_CHUNK) or -1
+    int n_tasks;
+    int *bn_nch;       // [n_big] chunks of big (chunked) net slot
+    int *bn_part0;     // [n_big] first partial of the slot
+    int n_big, n_parts;
     int *fin_pins;     // pins finished after the level loop (free pins, PI roots with out-arcs)
     int *fin_flags;    // 1 = accumulate onto the level-loop adjoint (root), 0 = fresh
     int n_fin;
@@ -66,12 +78,15 @@ struct Topo {
 
 // tq_flags
 constexpr int TQ_KIND = 3, TQ_ROOT_MEMBER = 4, TQ_TREE = 8, TQ_ROOT_EP = 16, TQ_ROOT_PI = 32,
-              TQ_BIG = 64;
+              TQ_MULTI_EP = 64;
 // tm_flags
-constexpr int TM_ROOT = 1, TM_EP = 2;
-// block partition: a "big" net (more than BIG_M members) gets a block of its
-// own; other blocks hold <= BLK_Q nets and <= BLK_M members
-constexpr int BIG_M = 32, BLK_Q = 64, BLK_M = 256, PASS_TPB = 256;
+constexpr int TM_ROOT = 1, TM_EP = 2, TM_MULTI_EP = 4;
+// task limits: one (item, cond) per thread of a 256-thread block
+constexpr int TASK_Q = 64, TASK_A = 64, TASK_M = 64, PASS_TPB = 256;
+// task flags: CHUNK = one chunk of a big star net's members; WIDE = one net
+// with more than TASK_A in-arcs; LOOP = one tree net with more than TASK_M
+// members (member phase loops, folds are sequential)
+constexpr int TK_CHUNK = 1, TK_WIDE = 2, TK_LOOP = 4;
 
 // Values and state of one corner.  (P,4) arrays are row-major 32-byte
 // records, exactly the reference's TimingState layout (sta.py:41-48).
@@ -87,6 +102,8 @@ struct Corner {
     double *red_tmp;   // pairwise-sum node values
     double *summary;   // [tns, wns, loss]
     unsigned *sync_ctr;  // last-block-done counter of the summary kernel
+    double *big_part;    // [n_parts * 8] per-chunk partial folds of big nets
+    unsigned *big_ctr;   // [n_big * 4] last-chunk-done counters (rc, hard, grad, fused)
 };
 
 struct LutView {

@@ -95,7 +95,7 @@ struct Context {
     std::vector<int> lv_ptr_host;     // L+1
     std::vector<int> lv_maxm_host;    // per level: max member count
     std::vector<int> lv_tree_host;    // per level: any tree net
-    std::vector<int> lvb_ptr_host;    // per level: first thread block (L+1)
+    std::vector<int> lvt_ptr_host;    // per level: first task (L+1)
     cudaStream_t s_main = nullptr, s_grad = nullptr;
     std::vector<cudaEvent_t> events;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_g1 = nullptr;

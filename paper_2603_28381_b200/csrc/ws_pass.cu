@@ -1,30 +1,34 @@
 // The differentiable STA pass on sm_100a (north_star items 2-5).
 //
-// Work layout: the level-major task arrays of ws_build.cu.  A level is a
-// contiguous range of thread blocks; a block owns <= BLK_Q nets (<= BLK_M
-// members), or one "big" net (> BIG_M members).  Every level kernel runs two
-// phases separated by one __syncthreads:
-//   forward : (net, cond) threads merge the in-arcs of their net (NLDM LUT
-//             interpolation against the shared-memory LUT pool; late max /
-//             early min with the first arc winning ties, then the winning
-//             arc's output slew; LSE smooth max for the late conditions),
-//             then (member, cond) threads write member arrival / slew / lse;
-//   backward: (member, cond) threads fold required times over out-arcs,
-//             write slack, gather adjoints (seed + d_arc of out-arcs), then
-//             (net, cond) threads fold the members into the root's required
-//             time and adjoint and emit d_arc = adjoint(root) * weight.
-// Each phase reads its task records with one coalesced load and gathers the
-// pin data it needs, so a level costs ~3 dependent memory round trips.
+// Work unit: a *task* (ws_build.cu build_tasks) = one thread block's share of
+// one level: <= 64 nets with <= 64 in-arcs and <= 64 members in total, so a
+// 256-thread block holds one (item, condition) per thread for each of the
+// three item kinds.  Every level kernel is three memory rounds deep:
+//   R1  the task record;
+//   R2  the nets' / arcs' / members' records (level-major task arrays, one
+//       coalesced load each);
+//   R3  every pin gather the task needs, all issued together (from-pin
+//       slew/arrival/lse, root load, member net_delay/impulse, out-arc
+//       required/arc_delay/d_arc, ...);
+// then compute in three block phases separated by __syncthreads:
+//   forward : (arc, cond) interpolate the delay LUT in shared memory and form
+//             arrival candidates -> (net, cond) merge them in arc order (late
+//             max / early min, first arc wins ties), interpolate the winner's
+//             slew LUT, LSE smooth max of the late conditions -> (member,
+//             cond) member arrival / slew / lse;
+//   backward: (member, cond) fold required times over out-arcs, slack,
+//             adjoint = seed + d_arc of out-arcs -> (net, cond) fold members
+//             into the root's required time and adjoint, emit d_arc.
+// Big star nets are split into chunks of 64 members (one task each; the last
+// chunk to finish combines the ordered partial folds); nets with > 64
+// in-arcs or big RC trees take a single-net task with sequential folds.
 //
-// Numerics: every fold keeps the reference's order (sequential per thread,
-// or an ordered tree where the earlier element wins ties), so the hard pass,
-// TNS and WNS equal the reference bit for bit; gradients equal it except for
-// the device exp/log ulps (and a blocked summation order for nets with more
-// than BIG_M members).
-//
-// Nothing is written twice: there is no init pass.  Each TimingState /
-// GradientState entry is produced by the kernel that finalizes it (members
-// and roots in the level kernels, pins in no net by k_free / k_fin).
+// Numerics: every fold keeps the reference's order (sequential, or an
+// ordered combine where the earlier element wins ties), so the hard pass,
+// TNS and WNS equal the reference bit for bit; gradients equal it up to the
+// device exp/log ulps (and a chunk-blocked sum order for nets with > 64
+// members).  Nothing is written twice: there is no init pass — each output
+// entry is produced by the kernel that finalizes it.
 #include <curand_kernel.h>
 #include <math.h>
 
@@ -44,68 +48,116 @@ namespace {
 
 constexpr double INF = __builtin_huge_val();
 
-// np.maximum.at / np.minimum.at merges of endpoint RATs into +-inf
-// (sta.py:55-67); early columns max, late columns min, NaN sticky.
-__device__ __forceinline__ double init_required(const Topo& t, const Corner& C, int pin, int c,
-                                                bool has_ep)
+struct Task {
+    int q0, nq, a0, na, m0, nm, flags, slot;
+};
+
+__device__ __forceinline__ Task load_task(const Topo& t, int k)
+{
+    const int4 a = t.tk_a[k], b = t.tk_b[k];
+    return Task{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
+
+// required-time init of a pin: np.maximum.at / np.minimum.at merges of its
+// endpoint RATs into -inf / +inf (sta.py:55-67); NaN sticky like numpy
+__device__ __forceinline__ double merge_req(double r, double x, int c)
+{
+    if (c < 2) return (r >= x || r != r) ? r : x;
+    return (r <= x || r != r) ? r : x;
+}
+
+__device__ double init_required_multi(const Topo& t, const Corner& C, int pin, int c)
 {
     double r = c < 2 ? -INF : INF;
-    if (has_ep)
-        for (int q = t.pin_ep_ptr[pin]; q < t.pin_ep_ptr[pin + 1]; q++) {
-            const double x = C.ep_required[(size_t)t.pin_ep_idx[q] * 4 + c];
-            if (c < 2) r = (r >= x || r != r) ? r : x;
-            else r = (r <= x || r != r) ? r : x;
-        }
+    for (int q = t.pin_ep_ptr[pin]; q < t.pin_ep_ptr[pin + 1]; q++)
+        r = merge_req(r, C.ep_required[(size_t)t.pin_ep_idx[q] * 4 + c], c);
     return r;
 }
 
-// endpoint-loss seed of a pin (diff.py:192-212): sum over its endpoint
-// entries, in entry order, of 1[v>0] (hinge) or sigmoid(v/gamma) (softplus)
-__device__ __forceinline__ double seed_adj(const Topo& t, const Corner& C, int pin, int j,
-                                           double lse_pin, double g, int kind)
+// endpoint-loss seed (diff.py:192-212): 1[v>0] (hinge) or sigmoid(v/gamma)
+__device__ __forceinline__ double seed_term(double v, double g, int kind)
+{
+    if (kind == 0) return v > 0.0 ? 1.0 : 0.0;
+    return __ddiv_rn(1.0, __dadd_rn(1.0, exp(__ddiv_rn(-v, g))));
+}
+
+__device__ double seed_multi(const Topo& t, const Corner& C, int pin, int j, double lse_pin,
+                             double g, int kind)
 {
     double a = 0.0;
-    for (int q = t.pin_ep_ptr[pin]; q < t.pin_ep_ptr[pin + 1]; q++) {
-        const double v = __dsub_rn(lse_pin, C.ep_required[(size_t)t.pin_ep_idx[q] * 4 + 2 + j]);
-        if (kind == 0) a = __dadd_rn(a, v > 0.0 ? 1.0 : 0.0);
-        else a = __dadd_rn(a, __ddiv_rn(1.0, __dadd_rn(1.0, exp(__ddiv_rn(-v, g)))));
-    }
+    for (int q = t.pin_ep_ptr[pin]; q < t.pin_ep_ptr[pin + 1]; q++)
+        a = __dadd_rn(a, seed_term(__dsub_rn(lse_pin, C.ep_required[(size_t)t.pin_ep_idx[q] * 4 + 2 + j]),
+                                   g, kind));
     return a;
 }
 
-// per-block copy of the task records of the block's nets
-struct BlockNets {
-    int q0, nq, m0, m1;
-    bool big;
-};
-
-__device__ __forceinline__ BlockNets block_nets(const Topo& t, int b, int* s_root, int* s_flags,
-                                                int* s_mptr, int* s_aptr, int* s_f0, int* s_net)
+__device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
 {
-    BlockNets B;
-    B.q0 = t.blk_q0[b];
-    B.nq = t.blk_q0[b + 1] - B.q0;
-    for (int i = threadIdx.x; i <= B.nq; i += blockDim.x) {
-        const int q = B.q0 + i;
-        s_mptr[i] = t.tq_mptr[q];
-        s_aptr[i] = t.tq_aptr[q];
-        if (i < B.nq) {
-            s_root[i] = t.tq_root[q];
-            s_flags[i] = t.tq_flags[q];
-            s_f0[i] = t.tq_f0[q];
-            s_net[i] = t.lv_nets[q];
-        }
-    }
-    __syncthreads();
-    B.m0 = s_mptr[0];
-    B.m1 = s_mptr[B.nq];
-    B.big = B.nq == 1 && (s_flags[0] & TQ_BIG);
-    return B;
+    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-#define WS_BLOCK_SMEM                                                              \
-    __shared__ int s_root[BLK_Q], s_flags[BLK_Q], s_f0[BLK_Q], s_net[BLK_Q];       \
-    __shared__ int s_mptr[BLK_Q + 1], s_aptr[BLK_Q + 1];
+// per-task copy of the nets' records
+struct NetSmem {
+    int root[TASK_Q], flags[TASK_Q], f0[TASK_Q], net[TASK_Q], e1[TASK_Q];
+    int aptr[TASK_Q + 1];   // absolute ta_* offsets
+    int mptr[TASK_Q + 1];   // absolute tm_* offsets
+};
+
+__device__ __forceinline__ void load_nets(const Topo& t, const Task& T, NetSmem& S)
+{
+    const int i = threadIdx.x;
+    if (i <= T.nq) {
+        const int q = T.q0 + i;
+        S.aptr[i] = t.tq_aptr[q];
+        S.mptr[i] = t.tq_mptr[q];
+        if (i < T.nq) {
+            S.root[i] = t.tq_root[q];
+            S.flags[i] = t.tq_flags[q];
+            S.f0[i] = t.tq_f0[q];
+            S.net[i] = t.lv_nets[q];
+            S.e1[i] = t.tq_e1[q];
+        }
+    }
+}
+
+// LSE of one arc-driven root, late column j = c - 2, read from global memory:
+// x_t = lse_at[from] + arc_delay; c = max x (first of equals);
+// s = z_0 + pairwise(z_1..) exactly like np.add.reduceat; weights z/s.
+__device__ double lse_root_global(const Topo& t, const Corner& C, int a0, int a1, int c, double g,
+                                  bool write_w)
+{
+    const int j = c - 2;
+    double cmax = -INF;
+    for (int q = a0; q < a1; q++) {
+        const double x = __dadd_rn(C.lse_at[(size_t)t.ta_from[q] * 2 + j],
+                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
+        if (q == a0 || x > cmax) cmax = x;
+    }
+    auto z_of = [&](int q) {
+        const double x = __dadd_rn(C.lse_at[(size_t)t.ta_from[q] * 2 + j],
+                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
+        return exp(__ddiv_rn(__dsub_rn(x, cmax), g));
+    };
+    const int n = a1 - a0;
+    double rest = 0.0;
+    if (n - 1 >= 8 && n - 1 <= 128) {     // numpy pairwise: 8 accumulators, then tail
+        double r[8];
+        for (int k = 0; k < 8; k++) r[k] = z_of(a0 + 1 + k);
+        int i = 8;
+        const int nn = n - 1;
+        for (; i < nn - (nn % 8); i += 8)
+            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], z_of(a0 + 1 + i + k));
+        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < nn; i++) rest = __dadd_rn(rest, z_of(a0 + 1 + i));
+    } else {                              // < 8 (numpy: sequential); > 129 in-arcs: sequential
+        for (int q = a0 + 1; q < a1; q++) rest = __dadd_rn(rest, z_of(q));
+    }
+    const double s = __dadd_rn(z_of(a0), rest);
+    if (write_w)
+        for (int q = a0; q < a1; q++) C.weights[(size_t)t.ta_arc[q] * 2 + j] = __ddiv_rn(z_of(q), s);
+    return __dadd_rn(cmax, __dmul_rn(g, log(s)));
+}
 
 // ---------------------------------------------------------------------------
 // pins in no net: their whole TimingState is the initial one (sta.py:51-68)
@@ -120,8 +172,7 @@ __global__ void k_free(Topo t, Corners cs, bool lse)
     const int pi = t.pin_pi[p];
     if (pi >= 0)
         for (int c = 0; c < 4; c++) { at[c] = C.pi_arrival[pi * 4 + c]; sl[c] = C.pi_slew[pi * 4 + c]; }
-    const bool ep = t.pin_ep_ptr[p + 1] > t.pin_ep_ptr[p];
-    for (int c = 0; c < 4; c++) rq[c] = init_required(t, C, p, c, ep);
+    for (int c = 0; c < 4; c++) rq[c] = init_required_multi(t, C, p, c);
     const double4 zero = make_double4(0, 0, 0, 0);
     reinterpret_cast<double4*>(C.load)[p] = zero;
     reinterpret_cast<double4*>(C.net_delay)[p] = zero;
@@ -136,8 +187,8 @@ __global__ void k_free(Topo t, Corners cs, bool lse)
 }
 
 // ---------------------------------------------------------------------------
-// RC (rc_level, _kernels.pyx:84-156) for every net in one launch: RC depends
-// only on values, so level order is irrelevant (sta.compute_rc).
+// RC (rc_level, _kernels.pyx:84-156).  RC depends only on values, so one
+// launch covers every task of every level (sta.compute_rc).
 
 // the reference's exact sequential algorithm for one (net, cond): tree nets
 // and reduce widths other than 8
@@ -182,373 +233,571 @@ __device__ void rc_seq(const Topo& t, const Corner& C, int net, int root, int s,
     }
 }
 
+// root load of a star net with reduce width 8: 8 strided partials summed
+// sequentially from 0.0, then p[l] += p[l+s] for s = 1, 2, 4
+__device__ __forceinline__ double root_load8(const double* caps, int stride, int m)
+{
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int base = 0; base < m; base += 8)
+#pragma unroll
+        for (int y = 0; y < 8; y++)
+            if (base + y < m) p[y] = __dadd_rn(p[y], caps[(size_t)(base + y) * stride]);
+    p[0] = __dadd_rn(p[0], p[1]); p[2] = __dadd_rn(p[2], p[3]);
+    p[4] = __dadd_rn(p[4], p[5]); p[6] = __dadd_rn(p[6], p[7]);
+    p[0] = __dadd_rn(p[0], p[2]); p[4] = __dadd_rn(p[4], p[6]);
+    return __dadd_rn(p[0], p[4]);
+}
+
+__device__ __forceinline__ bool last_chunk(unsigned* ctr, int nch, int* s_flag)
+{
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(ctr, 1u);
+        *s_flag = prev == (unsigned)(nch - 1);
+        if (*s_flag) *ctr = 0u;
+    }
+    __syncthreads();
+    if (*s_flag) __threadfence();
+    return *s_flag;
+}
+
 __global__ void __launch_bounds__(PASS_TPB) k_rc(Topo t, Corners cs, int w)
 {
     const Corner& C = cs.c[blockIdx.y];
-    WS_BLOCK_SMEM
-    __shared__ double s_cap[BLK_M * 4];
-    __shared__ double s_part[8 * 4];
-    const BlockNets B = block_nets(t, blockIdx.x, s_root, s_flags, s_mptr, s_aptr, s_f0, s_net);
+    __shared__ NetSmem S;
+    __shared__ double s_cap[TASK_M * 4];
+    __shared__ int s_flag;
+    const Task T = load_task(t, blockIdx.x);
+    const int tid = threadIdx.x;
     const bool fast = w == 8;
-    // phase A: members of star nets, one (member, cond) per thread
-    for (int i = threadIdx.x; i < (B.m1 - B.m0) * 4; i += blockDim.x) {
-        const int u = B.m0 + (i >> 2), c = i & 3;
-        const int fl = t.tm_flags[u], qi = fl >> 8;
-        if (!fast || (s_flags[qi] & TQ_TREE)) continue;
-        const size_t f = (size_t)(s_f0[qi] + (u - s_mptr[qi]));
+    // R2: records
+    load_nets(t, T, S);
+    int pin = 0, fl = 0;
+    const int mi = tid >> 2, c = tid & 3;
+    const bool mem_item = mi < T.nm && !(T.flags & TK_LOOP);
+    if (mem_item) {
+        pin = t.tm_pin[T.m0 + mi];
+        fl = t.tm_flags[T.m0 + mi];
+    }
+    __syncthreads();
+    // R3 + member phase (star nets, w == 8)
+    if (mem_item && fast && !(S.flags[fl >> 8] & TQ_TREE)) {
+        const int qi = fl >> 8;
+        const size_t f = (size_t)(S.f0[qi] + (T.m0 + mi - S.mptr[qi]));
         const double b = C.mem_cap[f * 4 + c];
         const double r = C.mem_res[f * 4 + c];
         const double d = __dadd_rn(0.0, __dmul_rn(r, b));
         const double rad = __dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, r), b), d), __dmul_rn(d, d));
-        const size_t pin = (size_t)t.tm_pin[u];
-        if (!(fl & TM_ROOT)) C.load[pin * 4 + c] = b;
-        C.net_delay[pin * 4 + c] = d;
-        C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
-        if (!B.big) s_cap[(u - B.m0) * 4 + c] = b;
+        if (!(fl & TM_ROOT)) C.load[(size_t)pin * 4 + c] = b;
+        C.net_delay[(size_t)pin * 4 + c] = d;
+        C.impulse[(size_t)pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+        s_cap[mi * 4 + c] = b;
     }
-    __syncthreads();
-    // phase B: root loads
-    if (!B.big) {
-        const int qi = threadIdx.x >> 2, c = threadIdx.x & 3;
-        if (qi >= B.nq) return;
-        const int fl = s_flags[qi], root = s_root[qi], net = s_net[qi];
-        const int k0 = s_mptr[qi] - B.m0, m = s_mptr[qi + 1] - s_mptr[qi];
-        if (!fast || (fl & TQ_TREE)) {
-            rc_seq(t, C, net, root, s_f0[qi], m, c, w, fl & TQ_ROOT_MEMBER);
+    if (T.flags & TK_CHUNK) {
+        // big star net: the last chunk sums every member's cap in order
+        const int root = S.root[0], net = S.net[0], s = S.f0[0];
+        const int m = S.mptr[1] - S.mptr[0];
+        if (!fast) {
+            if (last_chunk(C.big_ctr + 4 * T.slot + 0, t.bn_nch[T.slot], &s_flag) && tid < 4)
+                rc_seq(t, C, net, root, s, m, tid, w, S.flags[0] & TQ_ROOT_MEMBER);
             return;
         }
-        // 8 strided partials summed from 0.0, then p[l] += p[l+s], s = 1, 2, 4
-        double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int base = 0; base < m; base += 8)
-#pragma unroll
-            for (int y = 0; y < 8; y++)
-                if (base + y < m) p[y] = __dadd_rn(p[y], s_cap[(k0 + base + y) * 4 + c]);
-        p[0] = __dadd_rn(p[0], p[1]); p[2] = __dadd_rn(p[2], p[3]);
-        p[4] = __dadd_rn(p[4], p[5]); p[6] = __dadd_rn(p[6], p[7]);
-        p[0] = __dadd_rn(p[0], p[2]); p[4] = __dadd_rn(p[4], p[6]);
-        p[0] = __dadd_rn(p[0], p[4]);
-        C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], p[0]);
-        if (!(fl & TQ_ROOT_MEMBER)) {
-            C.net_delay[(size_t)root * 4 + c] = 0.0;
-            C.impulse[(size_t)root * 4 + c] = 0.0;
+        if (!last_chunk(C.big_ctr + 4 * T.slot + 0, t.bn_nch[T.slot], &s_flag)) return;
+        if (tid < 4) {
+            const double l = root_load8(C.mem_cap + (size_t)s * 4 + tid, 4, m);
+            C.load[(size_t)root * 4 + tid] = __dadd_rn(C.root_cap[(size_t)net * 4 + tid], l);
+            if (!(S.flags[0] & TQ_ROOT_MEMBER)) {
+                C.net_delay[(size_t)root * 4 + tid] = 0.0;
+                C.impulse[(size_t)root * 4 + tid] = 0.0;
+            }
         }
         return;
-    }
-    // big net: 32 threads (y, c) build the strided partials
-    const int fl = s_flags[0], root = s_root[0], net = s_net[0], s = s_f0[0];
-    const int m = B.m1 - B.m0;
-    if (!fast || (fl & TQ_TREE)) {
-        if (threadIdx.x < 4) rc_seq(t, C, net, root, s, m, threadIdx.x, w, fl & TQ_ROOT_MEMBER);
-        return;
-    }
-    if (threadIdx.x < 32) {
-        const int y = threadIdx.x >> 2, c = threadIdx.x & 3;
-        double p = 0.0;
-        for (int i = y; i < m; i += 8) p = __dadd_rn(p, C.mem_cap[(size_t)(s + i) * 4 + c]);
-        s_part[y * 4 + c] = p;
     }
     __syncthreads();
-    if (threadIdx.x < 4) {
-        const int c = threadIdx.x;
-        double* p = s_part;
-        const double p0 = __dadd_rn(p[0 * 4 + c], p[1 * 4 + c]), p2 = __dadd_rn(p[2 * 4 + c], p[3 * 4 + c]);
-        const double p4 = __dadd_rn(p[4 * 4 + c], p[5 * 4 + c]), p6 = __dadd_rn(p[6 * 4 + c], p[7 * 4 + c]);
-        const double tot = __dadd_rn(__dadd_rn(p0, p2), __dadd_rn(p4, p6));
-        C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], tot);
-        if (!(fl & TQ_ROOT_MEMBER)) {
-            C.net_delay[(size_t)root * 4 + c] = 0.0;
-            C.impulse[(size_t)root * 4 + c] = 0.0;
-        }
+    // net phase: root loads
+    const int qi = tid >> 2;
+    if (qi >= T.nq) return;
+    const int fq = S.flags[qi], root = S.root[qi], net = S.net[qi];
+    const int m = S.mptr[qi + 1] - S.mptr[qi];
+    if (!fast || (fq & TQ_TREE) || (T.flags & TK_LOOP)) {
+        rc_seq(t, C, net, root, S.f0[qi], m, c, w, fq & TQ_ROOT_MEMBER);
+        return;
+    }
+    const double l = root_load8(s_cap + (S.mptr[qi] - T.m0) * 4 + c, 4, m);
+    C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], l);
+    if (!(fq & TQ_ROOT_MEMBER)) {
+        C.net_delay[(size_t)root * 4 + c] = 0.0;
+        C.impulse[(size_t)root * 4 + c] = 0.0;
     }
 }
 
 // ---------------------------------------------------------------------------
 // forward level (forward_level, _kernels.pyx:159-210) + LSE (diff.py:123-146)
 
-__device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
-{
-    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
-}
-
-// LSE of one arc-driven root, late column j (cond c = j + 2):
-// x_t = lse_at[from] + arc_delay; c = max x (first of equals);
-// s = z_0 + pairwise(z_1..) exactly like np.add.reduceat; weights z/s.
-__device__ __forceinline__ double lse_root(const Topo& t, const Corner& C, int a0, int a1, int c,
-                                           double g)
-{
-    const int j = c - 2;
-    double cmax = -INF;
-    for (int q = a0; q < a1; q++) {
-        const double x = __dadd_rn(C.lse_at[(size_t)t.ta_from[q] * 2 + j],
-                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
-        if (q == a0 || x > cmax) cmax = x;
-    }
-    auto z_of = [&](int q) {
-        const double x = __dadd_rn(C.lse_at[(size_t)t.ta_from[q] * 2 + j],
-                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
-        return exp(__ddiv_rn(__dsub_rn(x, cmax), g));
-    };
-    const int n = a1 - a0;
-    double rest;
-    if (n - 1 < 8) {                       // numpy pairwise_sum, n < 8: sequential from 0.0
-        rest = 0.0;
-        for (int q = a0 + 1; q < a1; q++) rest = __dadd_rn(rest, z_of(q));
-    } else if (n - 1 <= 128) {             // 8 accumulators, combined pairwise, tail
-        double r[8];
-        for (int k = 0; k < 8; k++) r[k] = z_of(a0 + 1 + k);
-        int i = 8;
-        const int nn = n - 1;
-        for (; i < nn - (nn % 8); i += 8)
-            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], z_of(a0 + 1 + i + k));
-        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < nn; i++) rest = __dadd_rn(rest, z_of(a0 + 1 + i));
-    } else {                               // > 129 in-arcs: sequential (documented)
-        rest = 0.0;
-        for (int q = a0 + 1; q < a1; q++) rest = __dadd_rn(rest, z_of(q));
-    }
-    const double s = __dadd_rn(z_of(a0), rest);
-    for (int q = a0; q < a1; q++) C.weights[(size_t)t.ta_arc[q] * 2 + j] = __ddiv_rn(z_of(q), s);
-    return __dadd_rn(cmax, __dmul_rn(g, log(s)));
-}
+struct FwdSmem {
+    NetSmem n;
+    double cand[TASK_A * 4];    // arrival candidate of (arc, cond)
+    double slf[TASK_A * 4];     // slew at the arc's source
+    double x[TASK_A * 2];       // LSE operand of (arc, late col)
+    unsigned short slut[TASK_A * 4];
+    double ld[TASK_Q * 4];      // root load
+    double at[TASK_Q * 4], sl[TASK_Q * 4], lr[TASK_Q * 2];   // root results
+};
 
 template <bool HARD, bool LSE>
-__global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs, int b0,
+__global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
                                                   bool use_smem, double g)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ FwdSmem S;
     const Corner& C = cs.c[blockIdx.y];
-    WS_BLOCK_SMEM
-    __shared__ double s_at[BLK_Q * 4], s_sl[BLK_Q * 4], s_lr[BLK_Q * 2];
+    const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
+    const bool late = c >= 2;
+    const Task T = load_task(t, k0 + blockIdx.x);                       // R1
     LutView L;
     if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem);
-    const BlockNets B = block_nets(t, b0 + blockIdx.x, s_root, s_flags, s_mptr, s_aptr, s_f0, s_net);
-    // phase 1: one (net, cond) per thread
-    {
-        const int qi = threadIdx.x >> 2, c = threadIdx.x & 3;
-        if (qi < B.nq) {
-            const bool late = c >= 2;
-            const int root = s_root[qi], fl = s_flags[qi], kind = fl & TQ_KIND;
-            const int a0 = s_aptr[qi], a1 = s_aptr[qi + 1];
-            double at, sl, lr = 0.0;
-            if (kind == ROOT_ARC) {
+    const bool wide = T.flags & TK_WIDE;
+    // R2: records
+    load_nets(t, T, S.n);
+    const bool arc_item = ii < T.na && !wide;
+    int from = 0, root = 0, arc = 0, aq = 0;
+    ushort4 ld_ids{}, ls_ids{};
+    if (arc_item) {
+        const int q = T.a0 + ii;
+        from = t.ta_from[q];
+        root = t.ta_root[q];
+        arc = t.ta_arc[q];
+        aq = t.ta_q[q];
+        if (HARD) { ld_ids = t.ta_lut[2 * (size_t)q]; ls_ids = t.ta_lut[2 * (size_t)q + 1]; }
+    }
+    const bool mem_item = ii < T.nm;
+    int mpin = 0, mfl = 0;
+    if (mem_item) { mpin = t.tm_pin[T.m0 + ii]; mfl = t.tm_flags[T.m0 + ii]; }
+    // R3: gathers
+    double slf = 0, atf = 0, ld = 0, xl = 0, dd = 0;
+    if (arc_item) {
+        if (HARD) {
+            slf = C.slew[(size_t)from * 4 + c];
+            atf = C.arrival[(size_t)from * 4 + c];
+            ld = C.load[(size_t)root * 4 + c];
+        } else {
+            dd = C.arc_delay[(size_t)arc * 4 + c];
+        }
+        if (LSE && late) xl = C.lse_at[(size_t)from * 2 + (c - 2)];
+    }
+    double mnd = 0, mim = 0;
+    if (mem_item) {
+        mnd = C.net_delay[(size_t)mpin * 4 + c];
+        if (HARD) mim = C.impulse[(size_t)mpin * 4 + c];
+    }
+    __syncthreads();                  // LUT pool + net records visible
+    // arc phase
+    if (arc_item) {
+        if (HARD) {
+            dd = lut_interp(L, lut_c(ld_ids, c), slf, ld);
+            C.arc_delay[(size_t)arc * 4 + c] = dd;
+            S.cand[ii * 4 + c] = __dadd_rn(atf, dd);
+            S.slf[ii * 4 + c] = slf;
+            S.slut[ii * 4 + c] = lut_c(ls_ids, c);
+            S.ld[aq * 4 + c] = ld;
+        }
+        if (LSE && late) S.x[ii * 2 + (c - 2)] = __dadd_rn(xl, dd);
+    } else if (HARD && wide) {
+        // one net with > TASK_A in-arcs: arc delays in a loop, merge from global
+        const int rt = S.n.root[0];
+        for (int i = tid; i < T.na * 4; i += blockDim.x) {
+            const int q = T.a0 + (i >> 2), cc = i & 3;
+            const int fp = t.ta_from[q];
+            const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], cc),
+                                        C.slew[(size_t)fp * 4 + cc], C.load[(size_t)rt * 4 + cc]);
+            C.arc_delay[(size_t)t.ta_arc[q] * 4 + cc] = d;
+        }
+    }
+    __syncthreads();
+    // net phase: one (net, cond) per thread
+    const bool first = !(T.flags & TK_CHUNK) || T.m0 == S.n.mptr[0];
+    if (ii < T.nq) {
+        const int rt = S.n.root[ii], fl = S.n.flags[ii], kind = fl & TQ_KIND;
+        double at = 0, sl = 0, lr = 0;
+        if (kind == ROOT_ARC) {
+            const int a0 = S.n.aptr[ii] - T.a0, a1 = S.n.aptr[ii + 1] - T.a0;
+            if (!wide) {
                 if (HARD) {
-                    const double ld = C.load[(size_t)root * 4 + c];
                     double best = late ? -INF : INF;
                     int wq = a0;
                     for (int q = a0; q < a1; q++) {
-                        const int fp = t.ta_from[q];
-                        const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], c),
-                                                    C.slew[(size_t)fp * 4 + c], ld);
-                        C.arc_delay[(size_t)t.ta_arc[q] * 4 + c] = d;
-                        const double v = __dadd_rn(C.arrival[(size_t)fp * 4 + c], d);
+                        const double v = S.cand[q * 4 + c];
+                        if (later_wins(late, best, v)) { best = v; wq = q; }
+                    }
+                    at = best;
+                    sl = lut_interp(L, S.slut[wq * 4 + c], S.slf[wq * 4 + c], S.ld[ii * 4 + c]);
+                }
+                if (LSE && late) {
+                    const int j = c - 2;
+                    double cm = -INF;
+                    for (int q = a0; q < a1; q++) {
+                        const double x = S.x[q * 2 + j];
+                        if (q == a0 || x > cm) cm = x;
+                    }
+                    double z0 = 0.0, rest = 0.0;
+                    const int n = a1 - a0;
+                    if (n - 1 >= 8 && n - 1 <= 128) {
+                        // numpy pairwise leaf over z_1..z_{n-1}
+                        double r[8];
+                        for (int k = 0; k < 8; k++)
+                            r[k] = exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + k) * 2 + j], cm), g));
+                        int i = 8;
+                        const int nn = n - 1;
+                        for (; i < nn - (nn % 8); i += 8)
+                            for (int k = 0; k < 8; k++)
+                                r[k] = __dadd_rn(r[k], exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + i + k) * 2 + j], cm), g)));
+                        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+                        for (; i < nn; i++)
+                            rest = __dadd_rn(rest, exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + i) * 2 + j], cm), g)));
+                    } else {
+                        for (int q = a0 + 1; q < a1; q++)
+                            rest = __dadd_rn(rest, exp(__ddiv_rn(__dsub_rn(S.x[q * 2 + j], cm), g)));
+                    }
+                    z0 = exp(__ddiv_rn(__dsub_rn(S.x[a0 * 2 + j], cm), g));
+                    const double ssum = __dadd_rn(z0, rest);
+                    lr = __dadd_rn(cm, __dmul_rn(g, log(ssum)));
+                    if (first)
+                        for (int q = a0; q < a1; q++) {
+                            const double z = exp(__ddiv_rn(__dsub_rn(S.x[q * 2 + j], cm), g));
+                            C.weights[(size_t)t.ta_arc[T.a0 + q] * 2 + j] = __ddiv_rn(z, ssum);
+                        }
+                }
+            } else {
+                const int qa0 = S.n.aptr[0], qa1 = S.n.aptr[1];
+                if (HARD) {
+                    double best = late ? -INF : INF;
+                    int wq = qa0;
+                    for (int q = qa0; q < qa1; q++) {
+                        const double v = __dadd_rn(C.arrival[(size_t)t.ta_from[q] * 4 + c],
+                                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
                         if (later_wins(late, best, v)) { best = v; wq = q; }
                     }
                     at = best;
                     sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c),
-                                    C.slew[(size_t)t.ta_from[wq] * 4 + c], ld);
-                    C.arrival[(size_t)root * 4 + c] = at;
-                    C.slew[(size_t)root * 4 + c] = sl;
+                                    C.slew[(size_t)t.ta_from[wq] * 4 + c], C.load[(size_t)rt * 4 + c]);
                 }
-                if (LSE && late) {
-                    lr = lse_root(t, C, a0, a1, c, g);
-                    C.lse_at[(size_t)root * 2 + (c - 2)] = lr;
-                }
-            } else if (kind == ROOT_FEED) {
-                // driven by its parent net's member update (a lower level)
-                at = C.arrival[(size_t)root * 4 + c];
-                sl = C.slew[(size_t)root * 4 + c];
-                if (LSE && late) lr = C.lse_at[(size_t)root * 2 + (c - 2)];
-            } else {
-                // primary-input root (or undriven): the seeded values
-                at = 0.0;
-                sl = 0.0;
-                if (fl & TQ_ROOT_PI) {
-                    const int pi = t.pin_pi[root];
-                    at = C.pi_arrival[(size_t)pi * 4 + c];
-                    sl = C.pi_slew[(size_t)pi * 4 + c];
-                }
-                if (HARD) {
-                    C.arrival[(size_t)root * 4 + c] = at;
-                    C.slew[(size_t)root * 4 + c] = sl;
-                }
-                if (LSE && late) {
-                    lr = at;
-                    C.lse_at[(size_t)root * 2 + (c - 2)] = lr;
-                }
+                if (LSE && late) lr = lse_root_global(t, C, qa0, qa1, c, g, first);
             }
-            if (HARD) { s_at[qi * 4 + c] = at; s_sl[qi * 4 + c] = sl; }
-            if (LSE && late) s_lr[qi * 2 + (c - 2)] = lr;
+            if (first) {
+                if (HARD) {
+                    C.arrival[(size_t)rt * 4 + c] = at;
+                    C.slew[(size_t)rt * 4 + c] = sl;
+                }
+                if (LSE && late) C.lse_at[(size_t)rt * 2 + (c - 2)] = lr;
+            }
+        } else if (kind == ROOT_FEED) {
+            // driven by its parent net's member update (a lower level)
+            if (HARD) {
+                at = C.arrival[(size_t)rt * 4 + c];
+                sl = C.slew[(size_t)rt * 4 + c];
+            }
+            if (LSE && late) lr = C.lse_at[(size_t)rt * 2 + (c - 2)];
+        } else {
+            // primary-input root (or undriven): the seeded values
+            if (fl & TQ_ROOT_PI) {
+                const int pi = t.pin_pi[rt];
+                at = C.pi_arrival[(size_t)pi * 4 + c];
+                sl = C.pi_slew[(size_t)pi * 4 + c];
+            }
+            if (first) {
+                if (HARD) {
+                    C.arrival[(size_t)rt * 4 + c] = at;
+                    C.slew[(size_t)rt * 4 + c] = sl;
+                }
+                if (LSE && late) C.lse_at[(size_t)rt * 2 + (c - 2)] = at;
+            }
+            lr = at;
         }
+        S.at[ii * 4 + c] = at;
+        S.sl[ii * 4 + c] = sl;
+        if (late) S.lr[ii * 2 + (c - 2)] = lr;
     }
     __syncthreads();
-    // phase 2: one (member, cond) per thread
-    for (int i = threadIdx.x; i < (B.m1 - B.m0) * 4; i += blockDim.x) {
-        const int u = B.m0 + (i >> 2), c = i & 3;
-        const int qi = t.tm_flags[u] >> 8;
-        const size_t pin = (size_t)t.tm_pin[u];
-        const double nd = C.net_delay[pin * 4 + c];
-        if (HARD) {
-            const double sr = s_sl[qi * 4 + c], ii = C.impulse[pin * 4 + c];
-            C.arrival[pin * 4 + c] = __dadd_rn(s_at[qi * 4 + c], nd);
-            C.slew[pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(ii, ii)));
+    // member phase: one (member, cond) per thread
+    for (int i = tid; i < T.nm * 4; i += blockDim.x) {
+        int pin = mpin, fl = mfl;
+        double nd = mnd, im = mim;
+        if (i != tid) {       // TK_LOOP tasks only
+            pin = t.tm_pin[T.m0 + (i >> 2)];
+            fl = t.tm_flags[T.m0 + (i >> 2)];
+            nd = C.net_delay[(size_t)pin * 4 + c];
+            if (HARD) im = C.impulse[(size_t)pin * 4 + c];
         }
-        if (LSE && c >= 2) C.lse_at[pin * 2 + (c - 2)] = __dadd_rn(s_lr[qi * 2 + (c - 2)], nd);
+        const int qi = fl >> 8;
+        if (HARD) {
+            const double sr = S.sl[qi * 4 + c];
+            C.arrival[(size_t)pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], nd);
+            C.slew[(size_t)pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(im, im)));
+        }
+        if (LSE && late) C.lse_at[(size_t)pin * 2 + (c - 2)] = __dadd_rn(S.lr[qi * 2 + (c - 2)], nd);
     }
 }
 
 // ---------------------------------------------------------------------------
 // backward level (backward_level, _kernels.pyx:213-249) + reverse adjoint
-// (diff.py:215-241, gather form)
+// (diff.py:215-241 in gather form: a pin's adjoint is its seed plus the
+// d_arc of its out-arcs, read when the pin's own level runs)
+
+struct BwdSmem {
+    NetSmem n;
+    double v[TASK_M * 4];      // member required - net delay
+    double de[TASK_M * 2];     // member d_edge
+    double w[TASK_A * 2];      // in-arc softmax weights
+    int arc[TASK_A];
+    int flag;
+};
+
+// one member (u, c): fold required over out-arcs, slack, adjoint.
+template <bool HARD, bool GRAD>
+__device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int u, int pin, int fl,
+                                           int c, double g, int kind, double r0, double rto,
+                                           double ado, double nd, double at, double adj0,
+                                           double lse, double epl, double dout, double& v,
+                                           double& de)
+{
+    const int o0 = t.tm_optr[u], o1 = t.tm_optr[u + 1];
+    if (HARD) {
+        const bool mx = c < 2;
+        double r = r0;
+        if (o1 > o0) {
+            const double vv = __dsub_rn(rto, ado);
+            if (later_wins(mx, r, vv)) r = vv;
+            for (int o = o0 + 1; o < o1; o++) {
+                const double v2 = __dsub_rn(C.required[(size_t)t.to_to[o] * 4 + c],
+                                            C.arc_delay[(size_t)t.to_arc[o] * 4 + c]);
+                if (later_wins(mx, r, v2)) r = v2;
+            }
+        }
+        C.required[(size_t)pin * 4 + c] = r;
+        C.slack[(size_t)pin * 4 + c] = mx ? __dsub_rn(at, r) : __dsub_rn(r, at);
+        v = __dsub_rn(r, nd);
+    }
+    if (GRAD && c >= 2) {
+        const int j = c - 2;
+        double ad;
+        if (fl & TM_ROOT) ad = adj0;            // includes the seed (root fold, higher level)
+        else if (fl & TM_MULTI_EP) ad = seed_multi(t, C, pin, j, lse, g, kind);
+        else if (fl & TM_EP) ad = __dadd_rn(0.0, seed_term(__dsub_rn(lse, epl), g, kind));
+        else ad = 0.0;
+        if (o1 > o0) {
+            ad = __dadd_rn(ad, dout);
+            for (int o = o0 + 1; o < o1; o++) ad = __dadd_rn(ad, C.d_arc[(size_t)t.to_arc[o] * 2 + j]);
+        }
+        C.adjoint[(size_t)pin * 2 + j] = ad;
+        de = ad;
+    }
+}
 
 template <bool HARD, bool GRAD>
-__global__ void __launch_bounds__(PASS_TPB) k_bwd(Topo t, Corners cs, int b0, double g, int kind)
+__global__ void __launch_bounds__(PASS_TPB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
+                                                  int variant)
 {
+    __shared__ BwdSmem S;
     const Corner& C = cs.c[blockIdx.y];
-    WS_BLOCK_SMEM
-    __shared__ double s_v[BLK_M * 4], s_de[BLK_M * 2];
-    __shared__ double s_red[64 * 4];
-    const BlockNets B = block_nets(t, b0 + blockIdx.x, s_root, s_flags, s_mptr, s_aptr, s_f0, s_net);
-    // phase A: one (member, cond) per thread
-    for (int i = threadIdx.x; i < (B.m1 - B.m0) * 4; i += blockDim.x) {
-        const int u = B.m0 + (i >> 2), c = i & 3;
-        const int fl = t.tm_flags[u], qi = fl >> 8;
-        const size_t pin = (size_t)t.tm_pin[u];
-        const int o0 = t.tm_optr[u], o1 = t.tm_optr[u + 1];
-        const size_t f = (size_t)(s_f0[qi] + (u - s_mptr[qi]));
+    const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
+    const bool late = c >= 2;
+    const int j = c - 2;
+    const Task T = load_task(t, k0 + blockIdx.x);                       // R1
+    const bool loop = T.flags & TK_LOOP, chunk = T.flags & TK_CHUNK, wide = T.flags & TK_WIDE;
+    // R2: records
+    load_nets(t, T, S.n);
+    const bool mem_item = ii < T.nm;
+    const int u = T.m0 + ii;
+    int pin = 0, fl = 0, o1t = -1, o1a = -1, e1 = -1;
+    if (mem_item) {
+        pin = t.tm_pin[u];
+        fl = t.tm_flags[u];
+        o1t = t.tm_o1_to[u];
+        o1a = t.tm_o1_arc[u];
+        e1 = t.tm_e1[u];
+    }
+    const bool arc_item = GRAD && late && ii < T.na && !wide;
+    int arc = 0;
+    if (arc_item) arc = t.ta_arc[T.a0 + ii];
+    // R3: gathers
+    double r0 = 0, rto = 0, ado = 0, nd = 0, at = 0, adj0 = 0, lse = 0, epl = 0, dout = 0;
+    if (mem_item) {
         if (HARD) {
-            const bool mx = c < 2;
-            double r = (fl & TM_ROOT) ? C.required[pin * 4 + c]
-                                      : init_required(t, C, (int)pin, c, fl & TM_EP);
-            for (int o = o0; o < o1; o++) {
-                const double vv = __dsub_rn(C.required[(size_t)t.to_to[o] * 4 + c],
-                                            C.arc_delay[(size_t)t.to_arc[o] * 4 + c]);
-                if (later_wins(mx, r, vv)) r = vv;
+            if (fl & TM_ROOT) r0 = C.required[(size_t)pin * 4 + c];
+            else if (fl & TM_MULTI_EP) r0 = init_required_multi(t, C, pin, c);
+            else r0 = merge_req(c < 2 ? -INF : INF, (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c]
+                                                                : (c < 2 ? -INF : INF), c);
+            if (o1a >= 0) {
+                rto = C.required[(size_t)o1t * 4 + c];
+                ado = C.arc_delay[(size_t)o1a * 4 + c];
             }
-            C.required[pin * 4 + c] = r;
-            const double at = C.arrival[pin * 4 + c];
-            C.slack[pin * 4 + c] = mx ? __dsub_rn(at, r) : __dsub_rn(r, at);
-            const double v = __dsub_rn(r, C.net_delay[pin * 4 + c]);
-            if (B.big) C.mem_buf[f * 4 + c] = v;
-            else s_v[(u - B.m0) * 4 + c] = v;
+            nd = C.net_delay[(size_t)pin * 4 + c];
+            at = C.arrival[(size_t)pin * 4 + c];
         }
-        if (GRAD && c >= 2) {
-            const int j = c - 2;
-            double ad;
-            if (fl & TM_ROOT) ad = C.adjoint[pin * 2 + j];
-            else ad = (fl & TM_EP) ? seed_adj(t, C, (int)pin, j, C.lse_at[pin * 2 + j], g, kind) : 0.0;
-            for (int o = o0; o < o1; o++) ad = __dadd_rn(ad, C.d_arc[(size_t)t.to_arc[o] * 2 + j]);
-            C.adjoint[pin * 2 + j] = ad;
-            C.d_edge[f * 2 + j] = ad;
-            if (!B.big) s_de[(u - B.m0) * 2 + j] = ad;
+        if (GRAD && late) {
+            if (fl & TM_ROOT) adj0 = C.adjoint[(size_t)pin * 2 + j];
+            if (fl & TM_EP) {
+                lse = C.lse_at[(size_t)pin * 2 + j];
+                epl = C.ep_required[(size_t)e1 * 4 + 2 + j];
+            }
+            if (o1a >= 0) dout = C.d_arc[(size_t)o1a * 2 + j];
         }
     }
-    __syncthreads();
-    if (!B.big) {
-        // phase B: one (net, cond) per thread, members in order
-        const int qi = threadIdx.x >> 2, c = threadIdx.x & 3;
-        if (qi >= B.nq) return;
-        const int root = s_root[qi], fl = s_flags[qi];
-        const int k0 = s_mptr[qi] - B.m0, k1 = s_mptr[qi + 1] - B.m0;
-        if (HARD) {
-            const bool mx = c < 2;
-            double rr = init_required(t, C, root, c, fl & TQ_ROOT_EP);
-            for (int k = k0; k < k1; k++) {
-                const double v = s_v[k * 4 + c];
-                if (later_wins(mx, rr, v)) rr = v;
+    double wgt = 0;
+    if (arc_item) wgt = C.weights[(size_t)arc * 2 + j];
+    __syncthreads();                                   // net records visible
+    // member phase
+    for (int i = tid; i < T.nm * 4; i += blockDim.x) {
+        int uu = u, pp = pin, ff = fl;
+        double a_r0 = r0, a_rto = rto, a_ado = ado, a_nd = nd, a_at = at, a_adj0 = adj0,
+               a_lse = lse, a_epl = epl, a_dout = dout;
+        if (i != tid) {           // TK_LOOP tasks: later members load here
+            uu = T.m0 + (i >> 2);
+            pp = t.tm_pin[uu];
+            ff = t.tm_flags[uu];
+            const int ot = t.tm_o1_to[uu], oa = t.tm_o1_arc[uu], ee = t.tm_e1[uu];
+            if (HARD) {
+                a_r0 = (ff & TM_ROOT) ? C.required[(size_t)pp * 4 + c] : init_required_multi(t, C, pp, c);
+                if (oa >= 0) { a_rto = C.required[(size_t)ot * 4 + c]; a_ado = C.arc_delay[(size_t)oa * 4 + c]; }
+                a_nd = C.net_delay[(size_t)pp * 4 + c];
+                a_at = C.arrival[(size_t)pp * 4 + c];
             }
-            C.required[(size_t)root * 4 + c] = rr;
-            if (!(fl & TQ_ROOT_MEMBER)) {
-                const double at = C.arrival[(size_t)root * 4 + c];
-                C.slack[(size_t)root * 4 + c] = mx ? __dsub_rn(at, rr) : __dsub_rn(rr, at);
+            if (GRAD && late) {
+                if (ff & TM_ROOT) a_adj0 = C.adjoint[(size_t)pp * 2 + j];
+                if (ff & TM_EP) { a_lse = C.lse_at[(size_t)pp * 2 + j]; a_epl = C.ep_required[(size_t)ee * 4 + 2 + j]; }
+                if (oa >= 0) a_dout = C.d_arc[(size_t)oa * 2 + j];
             }
         }
-        if (GRAD && c >= 2) {
-            const int j = c - 2;
-            double ar = (fl & TQ_ROOT_EP)
-                            ? seed_adj(t, C, root, j, C.lse_at[(size_t)root * 2 + j], g, kind) : 0.0;
-            if (fl & TQ_TREE) {
-                // parents gather children, deepest member first (diff.py:222-233)
-                const int s = s_f0[qi];
-                for (int k = k1 - k0 - 1; k >= 0; k--) {
-                    const double dk = C.d_edge[(size_t)(s + k) * 2 + j];
-                    const int pl = t.mem_parent_loc[s + k];
-                    if (pl > 0) {
-                        double* dp = C.d_edge + (size_t)(s + pl - 1) * 2 + j;
-                        *dp = __dadd_rn(*dp, dk);
-                    } else {
-                        ar = __dadd_rn(ar, dk);
-                    }
-                }
-            } else {
-                for (int k = k1 - 1; k >= k0; k--) ar = __dadd_rn(ar, s_de[k * 2 + j]);
+        double v = 0, de = 0;
+        bwd_member<HARD, GRAD>(t, C, uu, pp, ff, c, g, kind, a_r0, a_rto, a_ado, a_nd, a_at, a_adj0,
+                               a_lse, a_epl, a_dout, v, de);
+        const int qi = ff >> 8;
+        const size_t f = (size_t)(S.n.f0[qi] + (uu - S.n.mptr[qi]));
+        if (HARD) {
+            if (loop) C.mem_buf[f * 4 + c] = v;
+            else S.v[(i >> 2) * 4 + c] = v;
+        }
+        if (GRAD && late) {
+            C.d_edge[f * 2 + j] = de;
+            if (!loop) S.de[(i >> 2) * 2 + j] = de;
+        }
+    }
+    if (arc_item) { S.w[ii * 2 + j] = wgt; S.arc[ii] = arc; }
+    __syncthreads();
+    if (chunk) {
+        // one chunk of a big star net: ordered partial folds, last chunk combines
+        const int nch = t.bn_nch[T.slot];
+        const int ch = (T.m0 - S.n.mptr[0]) / TASK_M;
+        double* part = C.big_part + (size_t)(t.bn_part0[T.slot] + ch) * 8;
+        if (tid < 4) {
+            if (HARD) {
+                const bool mx = c < 2;
+                double pr = mx ? -INF : INF;
+                for (int k = 0; k < T.nm; k++)
+                    if (later_wins(mx, pr, S.v[k * 4 + c])) pr = S.v[k * 4 + c];
+                part[c] = pr;
             }
-            C.adjoint[(size_t)root * 2 + j] = ar;
-            if ((fl & TQ_KIND) == ROOT_ARC)
-                for (int q = s_aptr[qi]; q < s_aptr[qi + 1]; q++) {
-                    const size_t a = (size_t)t.ta_arc[q];
-                    C.d_arc[a * 2 + j] = __dmul_rn(ar, C.weights[a * 2 + j]);
-                }
+            if (GRAD && late) {
+                double ps = 0.0;
+                for (int k = T.nm - 1; k >= 0; k--) ps = __dadd_rn(ps, S.de[k * 2 + j]);
+                part[4 + j] = ps;
+            }
+        }
+        if (!last_chunk(C.big_ctr + 4 * T.slot + variant, nch, &S.flag)) return;
+        if (tid >= 4) return;
+        const int rt = S.n.root[0], fq = S.n.flags[0];
+        const double* p0 = C.big_part + (size_t)t.bn_part0[T.slot] * 8;
+        if (HARD) {
+            const bool mx = c < 2;
+            double rr = (fq & TQ_MULTI_EP) ? init_required_multi(t, C, rt, c)
+                                           : merge_req(c < 2 ? -INF : INF,
+                                                       (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)S.n.e1[0] * 4 + c]
+                                                                         : (c < 2 ? -INF : INF), c);
+            for (int k = 0; k < nch; k++)
+                if (later_wins(mx, rr, p0[k * 8 + c])) rr = p0[k * 8 + c];
+            C.required[(size_t)rt * 4 + c] = rr;
+            if (!(fq & TQ_ROOT_MEMBER)) {
+                const double a = C.arrival[(size_t)rt * 4 + c];
+                C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
+            }
+        }
+        if (GRAD && late) {
+            double ar = 0.0;
+            if (fq & TQ_ROOT_EP) {
+                const double l = C.lse_at[(size_t)rt * 2 + j];
+                ar = (fq & TQ_MULTI_EP) ? seed_multi(t, C, rt, j, l, g, kind)
+                                        : __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)S.n.e1[0] * 4 + 2 + j]), g, kind));
+            }
+            for (int k = nch - 1; k >= 0; k--) ar = __dadd_rn(ar, p0[k * 8 + 4 + j]);
+            C.adjoint[(size_t)rt * 2 + j] = ar;
+            if ((fq & TQ_KIND) == ROOT_ARC)
+                for (int q = 0; q < T.na; q++)
+                    C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
         }
         return;
     }
-    // ---- one big net: ordered parallel folds over contiguous member ranges
-    const int root = s_root[0], fl = s_flags[0], s = s_f0[0], m = B.m1 - B.m0;
-    const int slot = threadIdx.x >> 2, c = threadIdx.x & 3;
-    const int per = (m + 63) / 64, k0 = min(m, slot * per), k1 = min(m, k0 + per);
+    // net phase: one (net, cond) per thread
+    if (ii >= T.nq) return;
+    const int rt = S.n.root[ii], fq = S.n.flags[ii];
+    const int k0m = S.n.mptr[ii] - T.m0, k1m = S.n.mptr[ii + 1] - T.m0;
     if (HARD) {
         const bool mx = c < 2;
-        double part = mx ? -INF : INF;
-        for (int k = k0; k < k1; k++) {
-            const double v = C.mem_buf[(size_t)(s + k) * 4 + c];
-            if (later_wins(mx, part, v)) part = v;
-        }
-        s_red[slot * 4 + c] = part;
-        __syncthreads();
-        if (slot == 0) {
-            double rr = init_required(t, C, root, c, fl & TQ_ROOT_EP);
-            for (int sl = 0; sl < 64; sl++)
-                if (later_wins(mx, rr, s_red[sl * 4 + c])) rr = s_red[sl * 4 + c];
-            C.required[(size_t)root * 4 + c] = rr;
-            if (!(fl & TQ_ROOT_MEMBER)) {
-                const double at = C.arrival[(size_t)root * 4 + c];
-                C.slack[(size_t)root * 4 + c] = mx ? __dsub_rn(at, rr) : __dsub_rn(rr, at);
+        double rr = (fq & TQ_MULTI_EP) ? init_required_multi(t, C, rt, c)
+                                       : merge_req(c < 2 ? -INF : INF,
+                                                   (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)S.n.e1[ii] * 4 + c]
+                                                                     : (c < 2 ? -INF : INF), c);
+        if (loop) {
+            const int s = S.n.f0[ii];
+            for (int k = 0; k < k1m - k0m; k++) {
+                const double v = C.mem_buf[(size_t)(s + k) * 4 + c];
+                if (later_wins(mx, rr, v)) rr = v;
             }
+        } else {
+            for (int k = k0m; k < k1m; k++)
+                if (later_wins(mx, rr, S.v[k * 4 + c])) rr = S.v[k * 4 + c];
         }
-        __syncthreads();
+        C.required[(size_t)rt * 4 + c] = rr;
+        if (!(fq & TQ_ROOT_MEMBER)) {
+            const double a = C.arrival[(size_t)rt * 4 + c];
+            C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
+        }
     }
-    if (GRAD) {
-        const int j = c - 2;
-        if (!(fl & TQ_TREE)) {
-            double part = 0.0;
-            if (c >= 2)
-                for (int k = k1 - 1; k >= k0; k--) part = __dadd_rn(part, C.d_edge[(size_t)(s + k) * 2 + j]);
-            s_red[slot * 4 + c] = part;
+    if (GRAD && late) {
+        double ar = 0.0;
+        if (fq & TQ_ROOT_EP) {
+            const double l = C.lse_at[(size_t)rt * 2 + j];
+            ar = (fq & TQ_MULTI_EP) ? seed_multi(t, C, rt, j, l, g, kind)
+                                    : __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)S.n.e1[ii] * 4 + 2 + j]), g, kind));
         }
-        __syncthreads();
-        if (slot == 0 && c >= 2) {
-            double ar = (fl & TQ_ROOT_EP)
-                            ? seed_adj(t, C, root, j, C.lse_at[(size_t)root * 2 + j], g, kind) : 0.0;
-            if (fl & TQ_TREE) {
-                for (int k = m - 1; k >= 0; k--) {
-                    const double dk = C.d_edge[(size_t)(s + k) * 2 + j];
-                    const int pl = t.mem_parent_loc[s + k];
-                    if (pl > 0) {
-                        double* dp = C.d_edge + (size_t)(s + pl - 1) * 2 + j;
-                        *dp = __dadd_rn(*dp, dk);
-                    } else {
-                        ar = __dadd_rn(ar, dk);
-                    }
+        if ((fq & TQ_TREE) || loop) {
+            // parents gather children, deepest member first (diff.py:222-233)
+            const int s = S.n.f0[ii];
+            for (int k = k1m - k0m - 1; k >= 0; k--) {
+                const double dk = C.d_edge[(size_t)(s + k) * 2 + j];
+                const int pl = (fq & TQ_TREE) ? t.mem_parent_loc[s + k] : 0;
+                if (pl > 0) {
+                    double* dp = C.d_edge + (size_t)(s + pl - 1) * 2 + j;
+                    *dp = __dadd_rn(*dp, dk);
+                } else {
+                    ar = __dadd_rn(ar, dk);
                 }
-            } else {
-                for (int sl = 63; sl >= 0; sl--) ar = __dadd_rn(ar, s_red[sl * 4 + c]);
             }
-            C.adjoint[(size_t)root * 2 + j] = ar;
-            if ((fl & TQ_KIND) == ROOT_ARC)
-                for (int q = s_aptr[0]; q < s_aptr[1]; q++) {
+        } else {
+            for (int k = k1m - 1; k >= k0m; k--) ar = __dadd_rn(ar, S.de[k * 2 + j]);
+        }
+        C.adjoint[(size_t)rt * 2 + j] = ar;
+        if ((fq & TQ_KIND) == ROOT_ARC) {
+            if (!wide) {
+                for (int q = S.n.aptr[ii] - T.a0; q < S.n.aptr[ii + 1] - T.a0; q++)
+                    C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
+            } else {
+                for (int q = S.n.aptr[0]; q < S.n.aptr[1]; q++) {
                     const size_t a = (size_t)t.ta_arc[q];
                     C.d_arc[a * 2 + j] = __dmul_rn(ar, C.weights[a * 2 + j]);
                 }
+            }
         }
     }
 }
@@ -562,7 +811,7 @@ __global__ void k_fin(Topo t, Corners cs, double g, int kind)
     if (i >= 2 * t.n_fin) return;
     const int p = t.fin_pins[i >> 1], j = i & 1;
     double ad = t.fin_flags[i >> 1] ? C.adjoint[(size_t)p * 2 + j]
-                                    : seed_adj(t, C, p, j, C.lse_at[(size_t)p * 2 + j], g, kind);
+                                    : seed_multi(t, C, p, j, C.lse_at[(size_t)p * 2 + j], g, kind);
     for (int q = t.pin_out_ptr[p]; q < t.pin_out_ptr[p + 1]; q++)
         ad = __dadd_rn(ad, C.d_arc[(size_t)t.pin_out_arc[q] * 2 + j]);
     C.adjoint[(size_t)p * 2 + j] = ad;
@@ -852,7 +1101,7 @@ struct Launcher {
         if (!use_smem) lut_bytes = 0;
     }
     dim3 grid1(int n, int tpb) const { return dim3((unsigned)std::max(1, (n + tpb - 1) / tpb), nc); }
-    int blocks(int li) const { return ctx.lvb_ptr_host[li + 1] - ctx.lvb_ptr_host[li]; }
+    int tasks(int li) const { return ctx.lvt_ptr_host[li + 1] - ctx.lvt_ptr_host[li]; }
 
     void free_pins(cudaStream_t s, bool lse)
     {
@@ -862,25 +1111,27 @@ struct Launcher {
     }
     void rc(cudaStream_t s, int w)
     {
-        if (!ctx.t.n_blocks) return;
-        k_rc<<<dim3(ctx.t.n_blocks, nc), PASS_TPB, 0, s>>>(ctx.t, cs, w);
+        if (!ctx.t.n_tasks) return;
+        k_rc<<<dim3(ctx.t.n_tasks, nc), PASS_TPB, 0, s>>>(ctx.t, cs, w);
         count++;
     }
     template <bool H, bool Lse>
     void fwd(cudaStream_t s, int li, double g)
     {
-        const int nb = blocks(li);
-        if (nb <= 0) return;
-        k_fwd<H, Lse><<<dim3(nb, nc), PASS_TPB, H ? lut_bytes : 0, s>>>(
-            ctx.t, ls, cs, ctx.lvb_ptr_host[li], use_smem, g);
+        const int nt = tasks(li);
+        if (nt <= 0) return;
+        k_fwd<H, Lse><<<dim3(nt, nc), PASS_TPB, H ? lut_bytes : 0, s>>>(
+            ctx.t, ls, cs, ctx.lvt_ptr_host[li], use_smem, g);
         count++;
     }
     template <bool H, bool G>
     void bwd(cudaStream_t s, int li, double g, int kind)
     {
-        const int nb = blocks(li);
-        if (nb <= 0) return;
-        k_bwd<H, G><<<dim3(nb, nc), PASS_TPB, 0, s>>>(ctx.t, cs, ctx.lvb_ptr_host[li], g, kind);
+        const int nt = tasks(li);
+        if (nt <= 0) return;
+        const int variant = H && G ? 3 : (H ? 1 : 2);
+        k_bwd<H, G><<<dim3(nt, nc), PASS_TPB, 0, s>>>(ctx.t, cs, ctx.lvt_ptr_host[li], g, kind,
+                                                      variant);
         count++;
     }
     void fin(cudaStream_t s, double g, int kind)
