@@ -182,7 +182,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--mode", default="fused", choices=("fused", "streams", "sequential"))
+    ap.add_argument("--mode", default="fused",
+                    choices=("persistent", "fused", "streams", "sequential"))
     ap.add_argument("--graph", type=int, default=1)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--workload", default="c3", choices=("c1", "c2", "c3"))
@@ -246,7 +247,8 @@ def main():
         f"device build {t_build * 1e3:.0f} ms")
 
     flags = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
-    flags |= {"fused": _lib.RUN_FUSED, "streams": _lib.RUN_TWO_STREAM, "sequential": 0}[args.mode]
+    flags |= {"persistent": _lib.RUN_PERSISTENT, "fused": _lib.RUN_FUSED,
+              "streams": _lib.RUN_TWO_STREAM, "sequential": 0}[args.mode]
     if args.graph:
         flags |= _lib.RUN_GRAPH
     stream = torch.cuda.current_stream()

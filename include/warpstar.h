@@ -108,7 +108,9 @@ enum ws_run_flags {
     WS_RUN_FUSED = 16u,      /* single stream, forward+LSE and backward+grad fused per level */
     WS_RUN_GRAPH = 32u,      /* capture the pass into a CUDA graph once, replay afterwards */
     WS_RUN_SUMMARY = 64u,    /* TNS/WNS (sta.py:408-421) from the corner's current slack */
-    WS_RUN_SLACK = 128u      /* slack (warp.py:474-475) from the current arrival/required */
+    WS_RUN_SLACK = 128u,     /* slack (warp.py:474-475) from the current arrival/required */
+    WS_RUN_PERSISTENT = 256u /* with HARD (and LSE|GRAD): the whole pass as one cooperative
+                                kernel, grid barrier between levels */
 };
 
 enum ws_loss_kind { WS_LOSS_HINGE = 0, WS_LOSS_SOFTPLUS = 1 };
@@ -147,6 +149,9 @@ int ws_device_ptr(ws_ctx *ctx, int corner, int field, void **dptr, int64_t *n_el
 int ws_value_ptr(ws_ctx *ctx, int corner, int field, void **dptr, int64_t *n_elems);
 /* out[0]=TNS out[1]=WNS out[2]=loss (synchronizes the stream) */
 int ws_summary(ws_ctx *ctx, int corner, double *out, void *stream);
+/* Profiling hook: device buffer receiving per-block phase timestamps in
+ * builds compiled with -DWS_PROBE (a no-op otherwise); NULL disables. */
+int ws_set_probe(ws_ctx *ctx, void *device_buf);
 /* number of kernels launched by the last ws_run */
 int ws_last_launch_count(ws_ctx *ctx);
 

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwarpstar_b200.so")
+LIB_PATH = os.environ.get("WS_LIB") or os.path.join(HERE, "libwarpstar_b200.so")
 
 WS_OK, WS_ERR_VALUE, WS_ERR_CYCLE, WS_ERR_NOMEM, WS_ERR_CUDA, WS_ERR_STATE = range(6)
 
@@ -40,6 +40,7 @@ TOPO = {name: i for i, name in enumerate(TOPO_FIELDS)}
 
 RUN_HARD, RUN_LSE, RUN_GRAD, RUN_TWO_STREAM, RUN_FUSED, RUN_GRAPH, RUN_SUMMARY, RUN_SLACK = (
     1, 2, 4, 8, 16, 32, 64, 128)
+RUN_PERSISTENT = 256
 LOSS_KINDS = {"hinge": 0, "softplus": 1}
 DIMS_LEN = 11
 
@@ -47,7 +48,7 @@ DIMS_LEN = 11
 EXPORTS = ("ws_abi_version", "ws_last_error", "ws_last_error_pin", "ws_create", "ws_destroy",
            "ws_dims", "ws_topology_len", "ws_get_topology", "ws_set_values",
            "ws_perturb_values", "ws_run", "ws_get", "ws_device_ptr", "ws_value_ptr",
-           "ws_summary", "ws_last_launch_count", "ws_set_state", "ws_rc_level", "ws_forward_level",
+           "ws_summary", "ws_last_launch_count", "ws_set_state", "ws_set_probe", "ws_rc_level", "ws_forward_level",
            "ws_backward_level")
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -115,6 +116,7 @@ def lib():
     L.ws_value_ptr.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp), _c_i64p]
     L.ws_summary.argtypes = [_vp, ctypes.c_int, _c_f64p, _vp]
     L.ws_last_launch_count.argtypes = [_vp]
+    L.ws_set_probe.argtypes = [_vp, _vp]
     i64, vp, d = ctypes.c_int64, _vp, ctypes.c_double
     L.ws_rc_level.argtypes = [i64, vp, i64, vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp,
                               ctypes.c_int]

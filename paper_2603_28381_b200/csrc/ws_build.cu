@@ -513,6 +513,9 @@ void build_tasks(Context& ctx)
     }
     ctx.lvt_ptr_host[t.L] = (int)ta_.size();
     t.n_tasks = (int)ta_.size();
+    t.lvt_ptr = ar.alloc<int>(t.L + 1);
+    WS_CUDA(cudaMemcpy(t.lvt_ptr, ctx.lvt_ptr_host.data(), sizeof(int) * (size_t)(t.L + 1),
+                       cudaMemcpyHostToDevice));
     t.tk_a = ar.alloc<int4>(ta_.size());
     t.tk_b = ar.alloc<int4>(tb_.size());
     if (!ta_.empty()) {
@@ -611,6 +614,33 @@ void build_topology(Context& ctx, const ws_design_desc* d)
     ctx.lut_t_len = (int)d->lut_t_len;
     t.lut_s_flat = upload(ar, d->lut_s_flat, d->lut_s_len, s);
     t.lut_l_flat = upload(ar, d->lut_l_flat, d->lut_l_len, s);
+    {
+        // canonical axis offsets: LUTs whose axis arrays hold identical values
+        // share one offset, so the level kernels locate a query once for both
+        // an arc's delay and slew tables (same result, bit for bit)
+        std::vector<int4> info((size_t)std::max<int64_t>(d->n_luts, 1));
+        auto canon = [](const double* flat, const int32_t* ptr, int64_t nl, std::vector<int>& out) {
+            out.assign((size_t)nl, 0);
+            for (int64_t i = 0; i < nl; i++) {
+                out[(size_t)i] = ptr[i];
+                const int n = ptr[i + 1] - ptr[i];
+                for (int64_t k = 0; k < i; k++)
+                    if (ptr[k + 1] - ptr[k] == n &&
+                        std::equal(flat + ptr[k], flat + ptr[k] + n, flat + ptr[i])) {
+                        out[(size_t)i] = out[(size_t)k];
+                        break;
+                    }
+            }
+        };
+        std::vector<int> cs_, cl_;
+        canon(d->lut_s_flat, d->lut_s_ptr, d->n_luts, cs_);
+        canon(d->lut_l_flat, d->lut_l_ptr, d->n_luts, cl_);
+        for (int64_t i = 0; i < d->n_luts; i++)
+            info[(size_t)i] = make_int4(cs_[(size_t)i], d->lut_s_ptr[i + 1] - d->lut_s_ptr[i],
+                                        cl_[(size_t)i], d->lut_l_ptr[i + 1] - d->lut_l_ptr[i]);
+        t.lut_info = upload(ar, info.data(), info.size(), s);
+        WS_CUDA(cudaStreamSynchronize(s));
+    }
 
     // ---- maps (flatten.py:190-206) --------------------------------------
     t.member_of_pin = ar.alloc<int>(P);

@@ -439,6 +439,14 @@ int ws_summary(ws_ctx* h, int corner, double* out, void* stream)
 
 int ws_last_launch_count(ws_ctx* h) { return h ? h->c.launches_last_run : -1; }
 
+int ws_set_probe(ws_ctx* h, void* device_buf)
+{
+    return guarded([&] {
+        if (!h) throw ws::Error(WS_ERR_VALUE, "null context");
+        h->c.t.probe = static_cast<unsigned long long*>(device_buf);
+    });
+}
+
 // ---------------------------------------------------------------------------
 // legacy per-level shims
 

@@ -10,6 +10,21 @@
 
 #define WS_FULL 0xffffffffu
 
+// WS_PROBE builds record globaltimer stamps at phase boundaries of block
+// (blockIdx.x) into t.probe[blockIdx.x * 8 + slot] (profiling only).
+#ifdef WS_PROBE
+#define WS_STAMP(t, slot)                                                                   \
+    do {                                                                                    \
+        if (threadIdx.x == 0 && (t).probe) {                                                \
+            unsigned long long _v;                                                          \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                          \
+            (t).probe[(size_t)blockIdx.x * 8 + (slot)] = _v;                                \
+        }                                                                                   \
+    } while (0)
+#else
+#define WS_STAMP(t, slot) do { } while (0)
+#endif
+
 namespace ws {
 
 constexpr int ROOT_ARC = 0, ROOT_PI = 1, ROOT_FEED = 2;
@@ -28,6 +43,7 @@ struct Topo {
     uint8_t *is_endpoint;
     int *lut_s_ptr, *lut_l_ptr, *lut_t_ptr;
     double *lut_s_flat, *lut_l_flat;
+    int4 *lut_info;    // canonical (deduplicated) axis offsets: s_off, nS, l_off, nL
     // level schedule (flatten.py:31-80): lv_nets = nets sorted by (level, id)
     int *level_of, *lv_ptr, *lv_nets;
     // derived work lists
@@ -68,9 +84,11 @@ struct Topo {
     int4 *tk_a;        // [T] q0, nq, a0, na
     int4 *tk_b;        // [T] m0, nm, flags (TK_*), big-net slot (TK_CHUNK) or -1
     int n_tasks;
+    int *lvt_ptr;      // [L+1] first task of each level
     int *bn_nch;       // [n_big] chunks of big (chunked) net slot
     int *bn_part0;     // [n_big] first partial of the slot
     int n_big, n_parts;
+    unsigned long long *probe;   // WS_PROBE builds: per-block phase timestamps
     int *fin_pins;     // pins finished after the level loop (free pins, PI roots with out-arcs)
     int *fin_flags;    // 1 = accumulate onto the level-loop adjoint (root), 0 = fresh
     int n_fin;
@@ -81,8 +99,10 @@ constexpr int TQ_KIND = 3, TQ_ROOT_MEMBER = 4, TQ_TREE = 8, TQ_ROOT_EP = 16, TQ_
               TQ_MULTI_EP = 64;
 // tm_flags
 constexpr int TM_ROOT = 1, TM_EP = 2, TM_MULTI_EP = 4;
-// task limits: one (item, cond) per thread of a 256-thread block
-constexpr int TASK_Q = 64, TASK_A = 64, TASK_M = 64, PASS_TPB = 256;
+// task limits: a 256-thread block holds one (net, cond) item and ITEMS
+// (arc, cond) / (member, cond) items per thread
+constexpr int PASS_TPB = 256, ITEMS = 2;
+constexpr int TASK_Q = PASS_TPB / 4, TASK_A = ITEMS * PASS_TPB / 4, TASK_M = ITEMS * PASS_TPB / 4;
 // task flags: CHUNK = one chunk of a big star net's members; WIDE = one net
 // with more than TASK_A in-arcs; LOOP = one tree net with more than TASK_M
 // members (member phase loops, folds are sequential)
@@ -109,6 +129,7 @@ struct Corner {
 struct LutView {
     const int *s_ptr, *l_ptr, *t_ptr;
     const double *s, *l, *t;
+    const int4 *info;   // per LUT: canonical slew-axis offset, nS, canonical load-axis offset, nL
 };
 
 // _kernels.pyx:15-81 / sta.py:79-113: upper_bound-1 clamped to [0,n-2],
@@ -152,6 +173,42 @@ __device__ __forceinline__ double lut_interp(const LutView& L, int lut, double q
     return __dadd_rn(__dmul_rn(1.0 - st, v0), __dmul_rn(st, v1));
 }
 
+// The same arithmetic split in two: locate a query on an axis (index and
+// clamped fraction), then blend a table at located positions.  An arc's
+// delay and slew tables share their axes in practice (the build dedupes
+// identical axis arrays), so one locate serves both.
+struct Loc {
+    int i0, i1;
+    double f;
+};
+
+__device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
+{
+    Loc r;
+    if (n > 1) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (ax[mid] <= q) lo = mid + 1; else hi = mid;
+        }
+        int i = lo - 1;
+        if (i < 0) i = 0; else if (i > n - 2) i = n - 2;
+        double t = (q - ax[i]) / (ax[i + 1] - ax[i]);
+        if (t < 0.0) t = 0.0; else if (t > 1.0) t = 1.0;
+        r.i0 = i; r.i1 = i + 1; r.f = t;
+    } else {
+        r.i0 = 0; r.i1 = 0; r.f = 0.0;
+    }
+    return r;
+}
+
+__device__ __forceinline__ double lut_blend(const double* tab, int nL, const Loc& s, const Loc& l)
+{
+    const double v0 = __dadd_rn(__dmul_rn(1.0 - l.f, tab[s.i0 * nL + l.i0]), __dmul_rn(l.f, tab[s.i0 * nL + l.i1]));
+    const double v1 = __dadd_rn(__dmul_rn(1.0 - l.f, tab[s.i1 * nL + l.i0]), __dmul_rn(l.f, tab[s.i1 * nL + l.i1]));
+    return __dadd_rn(__dmul_rn(1.0 - s.f, v0), __dmul_rn(s.f, v1));
+}
+
 // Ordered selection with the reference's strict comparisons: `cand` comes
 // later in the sequence than `cur`, so it wins only when strictly better
 // (first element wins ties, _kernels.pyx:195-197, 238-239, 247-248).
@@ -167,42 +224,48 @@ struct LutSrc {
     const int *s_ptr, *l_ptr, *t_ptr;
     const double *s, *l;
     int nl, s_len, l_len, t_len;
+    const int4 *info;
 };
 
 __host__ __device__ inline size_t lut_smem_bytes(int nl, int s_len, int l_len, int t_len)
 {
     size_t ints = 3 * (size_t)(nl + 1);
-    ints = (ints + 1) & ~(size_t)1;
-    return ints * 4 + (size_t)(s_len + l_len + t_len) * 8;
+    ints = (ints + 3) & ~(size_t)3;
+    return ints * 4 + (size_t)nl * 16 + (size_t)(s_len + l_len + t_len) * 8;
 }
 
 // Copies the pool (axes + this corner's tables) into smem when it fits
-// (use_smem), else views global memory.  Contains __syncthreads.
+// (use_smem), else views global memory.  Ends with __syncthreads unless
+// `sync` is false (the caller then owns the barrier before first use).
 __device__ __forceinline__ LutView stage_luts(const LutSrc& src, const double* t_flat,
-                                              bool use_smem, unsigned char* smem)
+                                              bool use_smem, unsigned char* smem, bool sync = true)
 {
     LutView v;
     if (!use_smem) {
         v.s_ptr = src.s_ptr; v.l_ptr = src.l_ptr; v.t_ptr = src.t_ptr;
-        v.s = src.s; v.l = src.l; v.t = t_flat;
+        v.s = src.s; v.l = src.l; v.t = t_flat; v.info = src.info;
         return v;
     }
     const int n1 = src.nl + 1;
     int* ip = reinterpret_cast<int*>(smem);
     size_t ints = 3 * (size_t)n1;
-    ints = (ints + 1) & ~(size_t)1;
-    double* dp = reinterpret_cast<double*>(smem + ints * 4);
+    ints = (ints + 3) & ~(size_t)3;
+    int4* inf = reinterpret_cast<int4*>(smem + ints * 4);
+    double* dp = reinterpret_cast<double*>(smem + ints * 4 + (size_t)src.nl * 16);
     for (int i = threadIdx.x; i < n1; i += blockDim.x) {
         ip[i] = src.s_ptr[i];
         ip[n1 + i] = src.l_ptr[i];
         ip[2 * n1 + i] = src.t_ptr[i];
     }
+    if (src.info)
+        for (int i = threadIdx.x; i < src.nl; i += blockDim.x) inf[i] = src.info[i];
     for (int i = threadIdx.x; i < src.s_len; i += blockDim.x) dp[i] = src.s[i];
     for (int i = threadIdx.x; i < src.l_len; i += blockDim.x) dp[src.s_len + i] = src.l[i];
     for (int i = threadIdx.x; i < src.t_len; i += blockDim.x) dp[src.s_len + src.l_len + i] = t_flat[i];
-    __syncthreads();
+    if (sync) __syncthreads();
     v.s_ptr = ip; v.l_ptr = ip + n1; v.t_ptr = ip + 2 * n1;
     v.s = dp; v.l = dp + src.s_len; v.t = dp + src.s_len + src.l_len;
+    v.info = inf;
     return v;
 }
 

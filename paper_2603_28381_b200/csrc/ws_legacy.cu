@@ -223,7 +223,7 @@ void launch_fwd_list(const Topo& t, const Corner* dcs, int n, int lut_s_len, int
 {
     if (n <= 0) return;
     LutSrc ls{t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, t.NL,
-              lut_s_len, lut_l_len, lut_t_len};
+              lut_s_len, lut_l_len, lut_t_len, nullptr};
     size_t bytes = lut_smem_bytes(t.NL, lut_s_len, lut_l_len, lut_t_len);
     const bool use_smem = bytes <= 48 * 1024;
     legacy::k_fwd<<<dim3((n + legacy::WPB - 1) / legacy::WPB, 1), legacy::NET_TPB, use_smem ? bytes : 0, s>>>(

@@ -96,6 +96,13 @@ __device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
+// Programmatic dependent launch (sm_90+): every pass kernel lets the next
+// kernel in the stream start launching immediately, runs its static prologue
+// (task record, topology records, LUT staging), and only then waits for the
+// previous kernel's results.  A no-op when launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // per-task copy of the nets' records
 struct NetSmem {
     int root[TASK_Q], flags[TASK_Q], f0[TASK_Q], net[TASK_Q], e1[TASK_Q];
@@ -162,11 +169,8 @@ __device__ double lse_root_global(const Topo& t, const Corner& C, int a0, int a1
 // ---------------------------------------------------------------------------
 // pins in no net: their whole TimingState is the initial one (sta.py:51-68)
 
-__global__ void k_free(Topo t, Corners cs, bool lse)
+__device__ void free_pin(const Topo& t, const Corner& C, int i, bool lse)
 {
-    const Corner& C = cs.c[blockIdx.y];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= t.n_free) return;
     const int p = t.free_pins[i];
     double at[4] = {0, 0, 0, 0}, sl[4] = {0, 0, 0, 0}, rq[4];
     const int pi = t.pin_pi[p];
@@ -184,6 +188,14 @@ __global__ void k_free(Topo t, Corners cs, bool lse)
         make_double4(__dsub_rn(at[0], rq[0]), __dsub_rn(at[1], rq[1]), __dsub_rn(rq[2], at[2]),
                      __dsub_rn(rq[3], at[3]));
     if (lse) reinterpret_cast<double2*>(C.lse_at)[p] = make_double2(at[2], at[3]);
+}
+
+__global__ void k_free(Topo t, Corners cs, bool lse)
+{
+    pdl_trigger();
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < t.n_free) free_pin(t, cs.c[blockIdx.y], i, lse);
 }
 
 // ---------------------------------------------------------------------------
@@ -262,166 +274,246 @@ __device__ __forceinline__ bool last_chunk(unsigned* ctr, int nch, int* s_flag)
     return *s_flag;
 }
 
-__global__ void __launch_bounds__(PASS_TPB) k_rc(Topo t, Corners cs, int w)
+// ---------------------------------------------------------------------------
+// Task bodies shared by the per-level kernels and the persistent kernel.
+// Each task kind is split into *records* (static topology: safe to load
+// before the previous level finished -> PDL prologue / prefetch before the
+// grid barrier) and *body* (gathers of the previous level's results and the
+// compute phases).  State written by other thread blocks during the pass is
+// read with ld.global.cg (L2), never through a possibly stale L1 line.
+
+#define LDG(p) __ldcg(p)
+
+// ---- RC --------------------------------------------------------------------
+
+struct RcSmem {
+    NetSmem n;
+    double cap[TASK_M * 4];
+    int flag;
+};
+
+struct RcRec {
+    int pin[ITEMS], fl[ITEMS];
+};
+
+__device__ __forceinline__ void rc_records(const Topo& t, const Task& T, RcSmem& S, RcRec& R)
 {
-    const Corner& C = cs.c[blockIdx.y];
-    __shared__ NetSmem S;
-    __shared__ double s_cap[TASK_M * 4];
-    __shared__ int s_flag;
-    const Task T = load_task(t, blockIdx.x);
-    const int tid = threadIdx.x;
-    const bool fast = w == 8;
-    // R2: records
-    load_nets(t, T, S);
-    int pin = 0, fl = 0;
-    const int mi = tid >> 2, c = tid & 3;
-    const bool mem_item = mi < T.nm && !(T.flags & TK_LOOP);
-    if (mem_item) {
-        pin = t.tm_pin[T.m0 + mi];
-        fl = t.tm_flags[T.m0 + mi];
+    load_nets(t, T, S.n);
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        const int mi = (threadIdx.x >> 2) + k * TASK_Q;
+        R.pin[k] = -1;
+        if (mi < T.nm && !(T.flags & TK_LOOP)) {
+            R.pin[k] = t.tm_pin[T.m0 + mi];
+            R.fl[k] = t.tm_flags[T.m0 + mi];
+        }
     }
-    __syncthreads();
-    // R3 + member phase (star nets, w == 8)
-    if (mem_item && fast && !(S.flags[fl >> 8] & TQ_TREE)) {
-        const int qi = fl >> 8;
-        const size_t f = (size_t)(S.f0[qi] + (T.m0 + mi - S.mptr[qi]));
+}
+
+__device__ void rc_body(const Topo& t, const Corner& C, const Task& T, RcSmem& S, const RcRec& R,
+                        int w)
+{
+    const int tid = threadIdx.x, c = tid & 3;
+    const bool fast = w == 8;
+    __syncthreads();                         // net records visible
+    // member phase (star nets, w == 8): one (member, cond) per item
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        const int mi = (tid >> 2) + k * TASK_Q;
+        if (R.pin[k] < 0) continue;
+        const int qi = R.fl[k] >> 8;
+        if (!fast || (S.n.flags[qi] & TQ_TREE)) continue;
+        const size_t f = (size_t)(S.n.f0[qi] + (T.m0 + mi - S.n.mptr[qi]));
         const double b = C.mem_cap[f * 4 + c];
         const double r = C.mem_res[f * 4 + c];
         const double d = __dadd_rn(0.0, __dmul_rn(r, b));
         const double rad = __dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, r), b), d), __dmul_rn(d, d));
-        if (!(fl & TM_ROOT)) C.load[(size_t)pin * 4 + c] = b;
-        C.net_delay[(size_t)pin * 4 + c] = d;
-        C.impulse[(size_t)pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
-        s_cap[mi * 4 + c] = b;
+        const size_t pin = (size_t)R.pin[k];
+        if (!(R.fl[k] & TM_ROOT)) C.load[pin * 4 + c] = b;
+        C.net_delay[pin * 4 + c] = d;
+        C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+        S.cap[mi * 4 + c] = b;
     }
     if (T.flags & TK_CHUNK) {
         // big star net: the last chunk sums every member's cap in order
-        const int root = S.root[0], net = S.net[0], s = S.f0[0];
-        const int m = S.mptr[1] - S.mptr[0];
-        if (!fast) {
-            if (last_chunk(C.big_ctr + 4 * T.slot + 0, t.bn_nch[T.slot], &s_flag) && tid < 4)
-                rc_seq(t, C, net, root, s, m, tid, w, S.flags[0] & TQ_ROOT_MEMBER);
-            return;
-        }
-        if (!last_chunk(C.big_ctr + 4 * T.slot + 0, t.bn_nch[T.slot], &s_flag)) return;
-        if (tid < 4) {
-            const double l = root_load8(C.mem_cap + (size_t)s * 4 + tid, 4, m);
-            C.load[(size_t)root * 4 + tid] = __dadd_rn(C.root_cap[(size_t)net * 4 + tid], l);
-            if (!(S.flags[0] & TQ_ROOT_MEMBER)) {
-                C.net_delay[(size_t)root * 4 + tid] = 0.0;
-                C.impulse[(size_t)root * 4 + tid] = 0.0;
+        const int root = S.n.root[0], net = S.n.net[0], s = S.n.f0[0];
+        const int m = S.n.mptr[1] - S.n.mptr[0];
+        const bool last = last_chunk(C.big_ctr + 4 * T.slot + 0, t.bn_nch[T.slot], &S.flag);
+        if (last && tid < 4) {
+            if (!fast) {
+                rc_seq(t, C, net, root, s, m, tid, w, S.n.flags[0] & TQ_ROOT_MEMBER);
+            } else {
+                const double l = root_load8(C.mem_cap + (size_t)s * 4 + tid, 4, m);
+                C.load[(size_t)root * 4 + tid] = __dadd_rn(C.root_cap[(size_t)net * 4 + tid], l);
+                if (!(S.n.flags[0] & TQ_ROOT_MEMBER)) {
+                    C.net_delay[(size_t)root * 4 + tid] = 0.0;
+                    C.impulse[(size_t)root * 4 + tid] = 0.0;
+                }
             }
         }
+        __syncthreads();
         return;
     }
     __syncthreads();
     // net phase: root loads
     const int qi = tid >> 2;
-    if (qi >= T.nq) return;
-    const int fq = S.flags[qi], root = S.root[qi], net = S.net[qi];
-    const int m = S.mptr[qi + 1] - S.mptr[qi];
-    if (!fast || (fq & TQ_TREE) || (T.flags & TK_LOOP)) {
-        rc_seq(t, C, net, root, S.f0[qi], m, c, w, fq & TQ_ROOT_MEMBER);
-        return;
+    if (qi < T.nq) {
+        const int fq = S.n.flags[qi], root = S.n.root[qi], net = S.n.net[qi];
+        const int m = S.n.mptr[qi + 1] - S.n.mptr[qi];
+        if (!fast || (fq & TQ_TREE) || (T.flags & TK_LOOP)) {
+            rc_seq(t, C, net, root, S.n.f0[qi], m, c, w, fq & TQ_ROOT_MEMBER);
+        } else {
+            const double l = root_load8(S.cap + (S.n.mptr[qi] - T.m0) * 4 + c, 4, m);
+            C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], l);
+            if (!(fq & TQ_ROOT_MEMBER)) {
+                C.net_delay[(size_t)root * 4 + c] = 0.0;
+                C.impulse[(size_t)root * 4 + c] = 0.0;
+            }
+        }
     }
-    const double l = root_load8(s_cap + (S.mptr[qi] - T.m0) * 4 + c, 4, m);
-    C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], l);
-    if (!(fq & TQ_ROOT_MEMBER)) {
-        C.net_delay[(size_t)root * 4 + c] = 0.0;
-        C.impulse[(size_t)root * 4 + c] = 0.0;
-    }
+    __syncthreads();                         // smem reusable by the next task
 }
 
-// ---------------------------------------------------------------------------
-// forward level (forward_level, _kernels.pyx:159-210) + LSE (diff.py:123-146)
+// ---- forward level (forward_level, _kernels.pyx:159-210) + LSE (diff.py:123-146)
 
 struct FwdSmem {
     NetSmem n;
     double cand[TASK_A * 4];    // arrival candidate of (arc, cond)
-    double slf[TASK_A * 4];     // slew at the arc's source
+    double sw[TASK_A * 4];      // output slew if the arc wins (speculative, parallel)
     double x[TASK_A * 2];       // LSE operand of (arc, late col)
-    unsigned short slut[TASK_A * 4];
-    double ld[TASK_Q * 4];      // root load
+    double z[TASK_A * 2];       // exp((x - c) / gamma)
+    double cm[TASK_Q * 2];      // LSE max per (net, late col)
+    double ss[TASK_Q * 2];      // LSE denominator
     double at[TASK_Q * 4], sl[TASK_Q * 4], lr[TASK_Q * 2];   // root results
 };
 
-template <bool HARD, bool LSE>
-__global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
-                                                  bool use_smem, double g)
+struct FwdRec {
+    int from[ITEMS], root[ITEMS], arc[ITEMS], aq[ITEMS];
+    unsigned short dl[ITEMS], sl[ITEMS];
+    int mpin[ITEMS], mfl[ITEMS];
+};
+
+// numpy's np.add.reduceat segment: z_0 + pairwise_sum(z_1 .. z_{n-1})
+__device__ __forceinline__ double reduceat_sum(const double* z, int stride, int n)
 {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ FwdSmem S;
-    const Corner& C = cs.c[blockIdx.y];
+    double rest = 0.0;
+    if (n - 1 >= 8 && n - 1 <= 128) {
+        double r[8];
+        for (int k = 0; k < 8; k++) r[k] = z[(1 + k) * stride];
+        int i = 8;
+        const int nn = n - 1;
+        for (; i < nn - (nn % 8); i += 8)
+            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], z[(1 + i + k) * stride]);
+        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < nn; i++) rest = __dadd_rn(rest, z[(1 + i) * stride]);
+    } else {   // numpy: sequential below 8; > 129 in-arcs: sequential (documented)
+        for (int q = 1; q < n; q++) rest = __dadd_rn(rest, z[q * stride]);
+    }
+    return __dadd_rn(z[0], rest);
+}
+
+template <bool HARD>
+__device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R)
+{
+    load_nets(t, T, S.n);
+    const int c = threadIdx.x & 3;
+    const bool wide = T.flags & TK_WIDE;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        const int ii = (threadIdx.x >> 2) + k * TASK_Q;
+        R.arc[k] = -1;
+        if (ii < T.na && !wide) {
+            const int q = T.a0 + ii;
+            R.from[k] = t.ta_from[q];
+            R.root[k] = t.ta_root[q];
+            R.arc[k] = t.ta_arc[q];
+            R.aq[k] = t.ta_q[q];
+            if (HARD) {
+                R.dl[k] = lut_c(t.ta_lut[2 * (size_t)q], c);
+                R.sl[k] = lut_c(t.ta_lut[2 * (size_t)q + 1], c);
+            }
+        }
+        R.mpin[k] = -1;
+        if (ii < T.nm) {
+            R.mpin[k] = t.tm_pin[T.m0 + ii];
+            R.mfl[k] = t.tm_flags[T.m0 + ii];
+        }
+    }
+}
+
+template <bool HARD, bool LSE>
+__device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const Task& T,
+                         FwdSmem& S, const FwdRec& R, double g)
+{
     const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
     const bool late = c >= 2;
-    const Task T = load_task(t, k0 + blockIdx.x);                       // R1
-    LutView L;
-    if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem);
+    const int j = c - 2;
     const bool wide = T.flags & TK_WIDE;
-    // R2: records
-    load_nets(t, T, S.n);
-    const bool arc_item = ii < T.na && !wide;
-    int from = 0, root = 0, arc = 0, aq = 0;
-    ushort4 ld_ids{}, ls_ids{};
-    if (arc_item) {
-        const int q = T.a0 + ii;
-        from = t.ta_from[q];
-        root = t.ta_root[q];
-        arc = t.ta_arc[q];
-        aq = t.ta_q[q];
-        if (HARD) { ld_ids = t.ta_lut[2 * (size_t)q]; ls_ids = t.ta_lut[2 * (size_t)q + 1]; }
-    }
-    const bool mem_item = ii < T.nm;
-    int mpin = 0, mfl = 0;
-    if (mem_item) { mpin = t.tm_pin[T.m0 + ii]; mfl = t.tm_flags[T.m0 + ii]; }
-    // R3: gathers
-    double slf = 0, atf = 0, ld = 0, xl = 0, dd = 0;
-    if (arc_item) {
-        if (HARD) {
-            slf = C.slew[(size_t)from * 4 + c];
-            atf = C.arrival[(size_t)from * 4 + c];
-            ld = C.load[(size_t)root * 4 + c];
-        } else {
-            dd = C.arc_delay[(size_t)arc * 4 + c];
+    // ---- R3: every gather of the task at once
+    double slf[ITEMS], atf[ITEMS], ld[ITEMS], xl[ITEMS], dd[ITEMS], mnd[ITEMS], mim[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        slf[k] = atf[k] = ld[k] = xl[k] = dd[k] = mnd[k] = mim[k] = 0.0;
+        if (R.arc[k] >= 0) {
+            if (HARD) {
+                slf[k] = LDG(C.slew + (size_t)R.from[k] * 4 + c);
+                atf[k] = LDG(C.arrival + (size_t)R.from[k] * 4 + c);
+                ld[k] = LDG(C.load + (size_t)R.root[k] * 4 + c);
+            } else {
+                dd[k] = LDG(C.arc_delay + (size_t)R.arc[k] * 4 + c);
+            }
+            if (LSE && late) xl[k] = LDG(C.lse_at + (size_t)R.from[k] * 2 + j);
         }
-        if (LSE && late) xl = C.lse_at[(size_t)from * 2 + (c - 2)];
-    }
-    double mnd = 0, mim = 0;
-    if (mem_item) {
-        mnd = C.net_delay[(size_t)mpin * 4 + c];
-        if (HARD) mim = C.impulse[(size_t)mpin * 4 + c];
-    }
-    __syncthreads();                  // LUT pool + net records visible
-    // arc phase
-    if (arc_item) {
-        if (HARD) {
-            dd = lut_interp(L, lut_c(ld_ids, c), slf, ld);
-            C.arc_delay[(size_t)arc * 4 + c] = dd;
-            S.cand[ii * 4 + c] = __dadd_rn(atf, dd);
-            S.slf[ii * 4 + c] = slf;
-            S.slut[ii * 4 + c] = lut_c(ls_ids, c);
-            S.ld[aq * 4 + c] = ld;
+        if (R.mpin[k] >= 0) {
+            mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
+            if (HARD) mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
         }
-        if (LSE && late) S.x[ii * 2 + (c - 2)] = __dadd_rn(xl, dd);
-    } else if (HARD && wide) {
+    }
+    __syncthreads();                  // net records (and the LUT pool) visible
+    // ---- arc phase: delay LUT, candidate, speculative output slew, LSE operand
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        if (R.arc[k] < 0) continue;
+        const int ai = ii + k * TASK_Q;
+        if (HARD) {
+            // delay and output-slew tables of this (arc, cond): one axis
+            // search serves both when their axes coincide
+            const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
+            const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
+            const Loc lld = lut_locate(L.l + di.z, di.w, ld[k]);
+            dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
+            const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
+            const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld[k]);
+            C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
+            S.cand[ai * 4 + c] = __dadd_rn(atf[k], dd[k]);
+            S.sw[ai * 4 + c] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
+        }
+        if (LSE && late) S.x[ai * 2 + j] = __dadd_rn(xl[k], dd[k]);
+    }
+    if (HARD && wide) {
         // one net with > TASK_A in-arcs: arc delays in a loop, merge from global
         const int rt = S.n.root[0];
         for (int i = tid; i < T.na * 4; i += blockDim.x) {
             const int q = T.a0 + (i >> 2), cc = i & 3;
             const int fp = t.ta_from[q];
             const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], cc),
-                                        C.slew[(size_t)fp * 4 + cc], C.load[(size_t)rt * 4 + cc]);
+                                        LDG(C.slew + (size_t)fp * 4 + cc), LDG(C.load + (size_t)rt * 4 + cc));
             C.arc_delay[(size_t)t.ta_arc[q] * 4 + cc] = d;
         }
     }
     __syncthreads();
-    // net phase: one (net, cond) per thread
+    // ---- net phase 1: merge in arc order (first arc wins ties), LSE max
     const bool first = !(T.flags & TK_CHUNK) || T.m0 == S.n.mptr[0];
+    int kind = 0, a0 = 0, a1 = 0, rt = 0;
     if (ii < T.nq) {
-        const int rt = S.n.root[ii], fl = S.n.flags[ii], kind = fl & TQ_KIND;
-        double at = 0, sl = 0, lr = 0;
+        const int fl = S.n.flags[ii];
+        kind = fl & TQ_KIND;
+        rt = S.n.root[ii];
+        a0 = S.n.aptr[ii] - T.a0;
+        a1 = S.n.aptr[ii + 1] - T.a0;
+        double at = 0, sl = 0;
         if (kind == ROOT_ARC) {
-            const int a0 = S.n.aptr[ii] - T.a0, a1 = S.n.aptr[ii + 1] - T.a0;
             if (!wide) {
                 if (HARD) {
                     double best = late ? -INF : INF;
@@ -431,43 +523,15 @@ __global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs,
                         if (later_wins(late, best, v)) { best = v; wq = q; }
                     }
                     at = best;
-                    sl = lut_interp(L, S.slut[wq * 4 + c], S.slf[wq * 4 + c], S.ld[ii * 4 + c]);
+                    sl = S.sw[wq * 4 + c];
                 }
                 if (LSE && late) {
-                    const int j = c - 2;
                     double cm = -INF;
                     for (int q = a0; q < a1; q++) {
                         const double x = S.x[q * 2 + j];
-                        if (q == a0 || x > cm) cm = x;
+                        if (q == a0 || x > cm) cm = x;   // np.maximum.reduceat
                     }
-                    double z0 = 0.0, rest = 0.0;
-                    const int n = a1 - a0;
-                    if (n - 1 >= 8 && n - 1 <= 128) {
-                        // numpy pairwise leaf over z_1..z_{n-1}
-                        double r[8];
-                        for (int k = 0; k < 8; k++)
-                            r[k] = exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + k) * 2 + j], cm), g));
-                        int i = 8;
-                        const int nn = n - 1;
-                        for (; i < nn - (nn % 8); i += 8)
-                            for (int k = 0; k < 8; k++)
-                                r[k] = __dadd_rn(r[k], exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + i + k) * 2 + j], cm), g)));
-                        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-                        for (; i < nn; i++)
-                            rest = __dadd_rn(rest, exp(__ddiv_rn(__dsub_rn(S.x[(a0 + 1 + i) * 2 + j], cm), g)));
-                    } else {
-                        for (int q = a0 + 1; q < a1; q++)
-                            rest = __dadd_rn(rest, exp(__ddiv_rn(__dsub_rn(S.x[q * 2 + j], cm), g)));
-                    }
-                    z0 = exp(__ddiv_rn(__dsub_rn(S.x[a0 * 2 + j], cm), g));
-                    const double ssum = __dadd_rn(z0, rest);
-                    lr = __dadd_rn(cm, __dmul_rn(g, log(ssum)));
-                    if (first)
-                        for (int q = a0; q < a1; q++) {
-                            const double z = exp(__ddiv_rn(__dsub_rn(S.x[q * 2 + j], cm), g));
-                            C.weights[(size_t)t.ta_arc[T.a0 + q] * 2 + j] = __ddiv_rn(z, ssum);
-                        }
+                    S.cm[ii * 2 + j] = cm;
                 }
             } else {
                 const int qa0 = S.n.aptr[0], qa1 = S.n.aptr[1];
@@ -475,30 +539,31 @@ __global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs,
                     double best = late ? -INF : INF;
                     int wq = qa0;
                     for (int q = qa0; q < qa1; q++) {
-                        const double v = __dadd_rn(C.arrival[(size_t)t.ta_from[q] * 4 + c],
-                                                   C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
+                        const double v = __dadd_rn(LDG(C.arrival + (size_t)t.ta_from[q] * 4 + c),
+                                                   LDG(C.arc_delay + (size_t)t.ta_arc[q] * 4 + c));
                         if (later_wins(late, best, v)) { best = v; wq = q; }
                     }
                     at = best;
                     sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c),
-                                    C.slew[(size_t)t.ta_from[wq] * 4 + c], C.load[(size_t)rt * 4 + c]);
+                                    LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), LDG(C.load + (size_t)rt * 4 + c));
                 }
-                if (LSE && late) lr = lse_root_global(t, C, qa0, qa1, c, g, first);
+                if (LSE && late) {
+                    const double lr = lse_root_global(t, C, qa0, qa1, c, g, first);
+                    S.lr[ii * 2 + j] = lr;
+                    if (first) C.lse_at[(size_t)rt * 2 + j] = lr;
+                }
             }
-            if (first) {
-                if (HARD) {
-                    C.arrival[(size_t)rt * 4 + c] = at;
-                    C.slew[(size_t)rt * 4 + c] = sl;
-                }
-                if (LSE && late) C.lse_at[(size_t)rt * 2 + (c - 2)] = lr;
+            if (first && HARD) {
+                C.arrival[(size_t)rt * 4 + c] = at;
+                C.slew[(size_t)rt * 4 + c] = sl;
             }
         } else if (kind == ROOT_FEED) {
             // driven by its parent net's member update (a lower level)
             if (HARD) {
-                at = C.arrival[(size_t)rt * 4 + c];
-                sl = C.slew[(size_t)rt * 4 + c];
+                at = LDG(C.arrival + (size_t)rt * 4 + c);
+                sl = LDG(C.slew + (size_t)rt * 4 + c);
             }
-            if (LSE && late) lr = C.lse_at[(size_t)rt * 2 + (c - 2)];
+            if (LSE && late) S.lr[ii * 2 + j] = LDG(C.lse_at + (size_t)rt * 2 + j);
         } else {
             // primary-input root (or undriven): the seeded values
             if (fl & TQ_ROOT_PI) {
@@ -511,37 +576,70 @@ __global__ void __launch_bounds__(PASS_TPB) k_fwd(Topo t, LutSrc ls, Corners cs,
                     C.arrival[(size_t)rt * 4 + c] = at;
                     C.slew[(size_t)rt * 4 + c] = sl;
                 }
-                if (LSE && late) C.lse_at[(size_t)rt * 2 + (c - 2)] = at;
+                if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = at;
             }
-            lr = at;
+            if (LSE && late) S.lr[ii * 2 + j] = at;
         }
-        S.at[ii * 4 + c] = at;
-        S.sl[ii * 4 + c] = sl;
-        if (late) S.lr[ii * 2 + (c - 2)] = lr;
+        if (HARD) { S.at[ii * 4 + c] = at; S.sl[ii * 4 + c] = sl; }
+    }
+    if (LSE && !wide) {
+        __syncthreads();
+        // ---- arc phase 2: z = exp((x - c) / gamma), all arcs in parallel
+        if (late)
+#pragma unroll
+            for (int k = 0; k < ITEMS; k++) {
+                if (R.arc[k] < 0) continue;
+                const int ai = ii + k * TASK_Q;
+                S.z[ai * 2 + j] = exp(__ddiv_rn(__dsub_rn(S.x[ai * 2 + j], S.cm[R.aq[k] * 2 + j]), g));
+            }
+        __syncthreads();
+        // ---- net phase 2: denominator and smooth max
+        if (ii < T.nq && late && kind == ROOT_ARC) {
+            const double s = reduceat_sum(S.z + a0 * 2 + j, 2, a1 - a0);
+            const double lr = __dadd_rn(S.cm[ii * 2 + j], __dmul_rn(g, log(s)));
+            S.ss[ii * 2 + j] = s;
+            S.lr[ii * 2 + j] = lr;
+            if (first) C.lse_at[(size_t)rt * 2 + j] = lr;
+        }
     }
     __syncthreads();
-    // member phase: one (member, cond) per thread
-    for (int i = tid; i < T.nm * 4; i += blockDim.x) {
-        int pin = mpin, fl = mfl;
-        double nd = mnd, im = mim;
-        if (i != tid) {       // TK_LOOP tasks only
-            pin = t.tm_pin[T.m0 + (i >> 2)];
-            fl = t.tm_flags[T.m0 + (i >> 2)];
-            nd = C.net_delay[(size_t)pin * 4 + c];
-            if (HARD) im = C.impulse[(size_t)pin * 4 + c];
+    // ---- arc phase 3: softmax weights (alongside the member phase)
+    if (LSE && !wide && first && late)
+#pragma unroll
+        for (int k = 0; k < ITEMS; k++) {
+            if (R.arc[k] < 0) continue;
+            const int ai = ii + k * TASK_Q;
+            C.weights[(size_t)R.arc[k] * 2 + j] = __ddiv_rn(S.z[ai * 2 + j], S.ss[R.aq[k] * 2 + j]);
         }
-        const int qi = fl >> 8;
+    // ---- member phase: one (member, cond) per item
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        if (R.mpin[k] < 0) continue;
+        const size_t pin = (size_t)R.mpin[k];
+        const int qi = R.mfl[k] >> 8;
         if (HARD) {
             const double sr = S.sl[qi * 4 + c];
-            C.arrival[(size_t)pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], nd);
-            C.slew[(size_t)pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(im, im)));
+            C.arrival[pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], mnd[k]);
+            C.slew[pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(mim[k], mim[k])));
         }
-        if (LSE && late) C.lse_at[(size_t)pin * 2 + (c - 2)] = __dadd_rn(S.lr[qi * 2 + (c - 2)], nd);
+        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[qi * 2 + j], mnd[k]);
     }
+    for (int i = tid + ITEMS * PASS_TPB; i < T.nm * 4; i += blockDim.x) {   // TK_LOOP tasks
+        const int u = T.m0 + (i >> 2);
+        const size_t pin = (size_t)t.tm_pin[u];
+        const int qi = t.tm_flags[u] >> 8;
+        const double nd = LDG(C.net_delay + pin * 4 + c);
+        if (HARD) {
+            const double sr = S.sl[qi * 4 + c], im = LDG(C.impulse + pin * 4 + c);
+            C.arrival[pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], nd);
+            C.slew[pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(im, im)));
+        }
+        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[qi * 2 + j], nd);
+    }
+    __syncthreads();                         // smem reusable by the next task
 }
 
-// ---------------------------------------------------------------------------
-// backward level (backward_level, _kernels.pyx:213-249) + reverse adjoint
+// ---- backward level (backward_level, _kernels.pyx:213-249) + reverse adjoint
 // (diff.py:215-241 in gather form: a pin's adjoint is its seed plus the
 // d_arc of its out-arcs, read when the pin's own level runs)
 
@@ -553,6 +651,32 @@ struct BwdSmem {
     int arc[TASK_A];
     int flag;
 };
+
+struct BwdRec {
+    int pin[ITEMS], fl[ITEMS], o1t[ITEMS], o1a[ITEMS], e1[ITEMS], arc[ITEMS];
+};
+
+template <bool GRAD>
+__device__ __forceinline__ void bwd_records(const Topo& t, const Task& T, BwdSmem& S, BwdRec& R)
+{
+    load_nets(t, T, S.n);
+    const bool late = (threadIdx.x & 3) >= 2;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        const int ii = (threadIdx.x >> 2) + k * TASK_Q;
+        R.pin[k] = -1;
+        if (ii < T.nm) {
+            const int u = T.m0 + ii;
+            R.pin[k] = t.tm_pin[u];
+            R.fl[k] = t.tm_flags[u];
+            R.o1t[k] = t.tm_o1_to[u];
+            R.o1a[k] = t.tm_o1_arc[u];
+            R.e1[k] = t.tm_e1[u];
+        }
+        R.arc[k] = -1;
+        if (GRAD && late && ii < T.na && !(T.flags & TK_WIDE)) R.arc[k] = t.ta_arc[T.a0 + ii];
+    }
+}
 
 // one member (u, c): fold required over out-arcs, slack, adjoint.
 template <bool HARD, bool GRAD>
@@ -570,8 +694,8 @@ __device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int u
             const double vv = __dsub_rn(rto, ado);
             if (later_wins(mx, r, vv)) r = vv;
             for (int o = o0 + 1; o < o1; o++) {
-                const double v2 = __dsub_rn(C.required[(size_t)t.to_to[o] * 4 + c],
-                                            C.arc_delay[(size_t)t.to_arc[o] * 4 + c]);
+                const double v2 = __dsub_rn(LDG(C.required + (size_t)t.to_to[o] * 4 + c),
+                                            LDG(C.arc_delay + (size_t)t.to_arc[o] * 4 + c));
                 if (later_wins(mx, r, v2)) r = v2;
             }
         }
@@ -588,7 +712,7 @@ __device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int u
         else ad = 0.0;
         if (o1 > o0) {
             ad = __dadd_rn(ad, dout);
-            for (int o = o0 + 1; o < o1; o++) ad = __dadd_rn(ad, C.d_arc[(size_t)t.to_arc[o] * 2 + j]);
+            for (int o = o0 + 1; o < o1; o++) ad = __dadd_rn(ad, LDG(C.d_arc + (size_t)t.to_arc[o] * 2 + j));
         }
         C.adjoint[(size_t)pin * 2 + j] = ad;
         de = ad;
@@ -596,95 +720,111 @@ __device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int u
 }
 
 template <bool HARD, bool GRAD>
-__global__ void __launch_bounds__(PASS_TPB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
-                                                  int variant)
+__device__ __forceinline__ void bwd_gather(const Corner& C, int pin, int fl, int o1t, int o1a,
+                                           int e1, int c, const Topo& t, double& r0, double& rto,
+                                           double& ado, double& nd, double& at, double& adj0,
+                                           double& lse, double& epl, double& dout)
 {
-    __shared__ BwdSmem S;
-    const Corner& C = cs.c[blockIdx.y];
+    const int j = c - 2;
+    if (HARD) {
+        if (fl & TM_ROOT) r0 = LDG(C.required + (size_t)pin * 4 + c);
+        else if (fl & TM_MULTI_EP) r0 = init_required_multi(t, C, pin, c);
+        else r0 = merge_req(c < 2 ? -INF : INF, (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c]
+                                                            : (c < 2 ? -INF : INF), c);
+        if (o1a >= 0) {
+            rto = LDG(C.required + (size_t)o1t * 4 + c);
+            ado = LDG(C.arc_delay + (size_t)o1a * 4 + c);
+        }
+        nd = LDG(C.net_delay + (size_t)pin * 4 + c);
+        at = LDG(C.arrival + (size_t)pin * 4 + c);
+    }
+    if (GRAD && c >= 2) {
+        if (fl & TM_ROOT) adj0 = LDG(C.adjoint + (size_t)pin * 2 + j);
+        if (fl & TM_EP) {
+            lse = LDG(C.lse_at + (size_t)pin * 2 + j);
+            epl = C.ep_required[(size_t)e1 * 4 + 2 + j];
+        }
+        if (o1a >= 0) dout = LDG(C.d_arc + (size_t)o1a * 2 + j);
+    }
+}
+
+__device__ __forceinline__ double root_init_required(const Topo& t, const Corner& C, int rt, int fq,
+                                                      int e1, int c)
+{
+    if (fq & TQ_MULTI_EP) return init_required_multi(t, C, rt, c);
+    return merge_req(c < 2 ? -INF : INF,
+                     (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)e1 * 4 + c] : (c < 2 ? -INF : INF), c);
+}
+
+__device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int rt, int fq, int e1,
+                                            int j, double g, int kind)
+{
+    if (!(fq & TQ_ROOT_EP)) return 0.0;
+    const double l = LDG(C.lse_at + (size_t)rt * 2 + j);
+    if (fq & TQ_MULTI_EP) return seed_multi(t, C, rt, j, l, g, kind);
+    return __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)e1 * 4 + 2 + j]), g, kind));
+}
+
+template <bool HARD, bool GRAD>
+__device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem& S,
+                         const BwdRec& R, double g, int kind, int variant)
+{
     const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
     const bool late = c >= 2;
     const int j = c - 2;
-    const Task T = load_task(t, k0 + blockIdx.x);                       // R1
     const bool loop = T.flags & TK_LOOP, chunk = T.flags & TK_CHUNK, wide = T.flags & TK_WIDE;
-    // R2: records
-    load_nets(t, T, S.n);
-    const bool mem_item = ii < T.nm;
-    const int u = T.m0 + ii;
-    int pin = 0, fl = 0, o1t = -1, o1a = -1, e1 = -1;
-    if (mem_item) {
-        pin = t.tm_pin[u];
-        fl = t.tm_flags[u];
-        o1t = t.tm_o1_to[u];
-        o1a = t.tm_o1_arc[u];
-        e1 = t.tm_e1[u];
+    // ---- R3: gathers
+    double r0[ITEMS], rto[ITEMS], ado[ITEMS], nd[ITEMS], at[ITEMS], adj0[ITEMS], lse[ITEMS],
+        epl[ITEMS], dout[ITEMS], wgt[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        r0[k] = rto[k] = ado[k] = nd[k] = at[k] = adj0[k] = lse[k] = epl[k] = dout[k] = wgt[k] = 0.0;
+        if (R.pin[k] >= 0)
+            bwd_gather<HARD, GRAD>(C, R.pin[k], R.fl[k], R.o1t[k], R.o1a[k], R.e1[k], c, t, r0[k],
+                                   rto[k], ado[k], nd[k], at[k], adj0[k], lse[k], epl[k], dout[k]);
+        if (R.arc[k] >= 0) wgt[k] = LDG(C.weights + (size_t)R.arc[k] * 2 + j);
     }
-    const bool arc_item = GRAD && late && ii < T.na && !wide;
-    int arc = 0;
-    if (arc_item) arc = t.ta_arc[T.a0 + ii];
-    // R3: gathers
-    double r0 = 0, rto = 0, ado = 0, nd = 0, at = 0, adj0 = 0, lse = 0, epl = 0, dout = 0;
-    if (mem_item) {
-        if (HARD) {
-            if (fl & TM_ROOT) r0 = C.required[(size_t)pin * 4 + c];
-            else if (fl & TM_MULTI_EP) r0 = init_required_multi(t, C, pin, c);
-            else r0 = merge_req(c < 2 ? -INF : INF, (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c]
-                                                                : (c < 2 ? -INF : INF), c);
-            if (o1a >= 0) {
-                rto = C.required[(size_t)o1t * 4 + c];
-                ado = C.arc_delay[(size_t)o1a * 4 + c];
-            }
-            nd = C.net_delay[(size_t)pin * 4 + c];
-            at = C.arrival[(size_t)pin * 4 + c];
-        }
-        if (GRAD && late) {
-            if (fl & TM_ROOT) adj0 = C.adjoint[(size_t)pin * 2 + j];
-            if (fl & TM_EP) {
-                lse = C.lse_at[(size_t)pin * 2 + j];
-                epl = C.ep_required[(size_t)e1 * 4 + 2 + j];
-            }
-            if (o1a >= 0) dout = C.d_arc[(size_t)o1a * 2 + j];
-        }
-    }
-    double wgt = 0;
-    if (arc_item) wgt = C.weights[(size_t)arc * 2 + j];
     __syncthreads();                                   // net records visible
-    // member phase
-    for (int i = tid; i < T.nm * 4; i += blockDim.x) {
-        int uu = u, pp = pin, ff = fl;
-        double a_r0 = r0, a_rto = rto, a_ado = ado, a_nd = nd, a_at = at, a_adj0 = adj0,
-               a_lse = lse, a_epl = epl, a_dout = dout;
-        if (i != tid) {           // TK_LOOP tasks: later members load here
-            uu = T.m0 + (i >> 2);
-            pp = t.tm_pin[uu];
-            ff = t.tm_flags[uu];
-            const int ot = t.tm_o1_to[uu], oa = t.tm_o1_arc[uu], ee = t.tm_e1[uu];
-            if (HARD) {
-                a_r0 = (ff & TM_ROOT) ? C.required[(size_t)pp * 4 + c] : init_required_multi(t, C, pp, c);
-                if (oa >= 0) { a_rto = C.required[(size_t)ot * 4 + c]; a_ado = C.arc_delay[(size_t)oa * 4 + c]; }
-                a_nd = C.net_delay[(size_t)pp * 4 + c];
-                a_at = C.arrival[(size_t)pp * 4 + c];
-            }
-            if (GRAD && late) {
-                if (ff & TM_ROOT) a_adj0 = C.adjoint[(size_t)pp * 2 + j];
-                if (ff & TM_EP) { a_lse = C.lse_at[(size_t)pp * 2 + j]; a_epl = C.ep_required[(size_t)ee * 4 + 2 + j]; }
-                if (oa >= 0) a_dout = C.d_arc[(size_t)oa * 2 + j];
-            }
-        }
+    // ---- member phase
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        if (R.pin[k] < 0) continue;
+        const int mi = ii + k * TASK_Q, u = T.m0 + mi;
         double v = 0, de = 0;
-        bwd_member<HARD, GRAD>(t, C, uu, pp, ff, c, g, kind, a_r0, a_rto, a_ado, a_nd, a_at, a_adj0,
-                               a_lse, a_epl, a_dout, v, de);
-        const int qi = ff >> 8;
-        const size_t f = (size_t)(S.n.f0[qi] + (uu - S.n.mptr[qi]));
+        bwd_member<HARD, GRAD>(t, C, u, R.pin[k], R.fl[k], c, g, kind, r0[k], rto[k], ado[k], nd[k],
+                               at[k], adj0[k], lse[k], epl[k], dout[k], v, de);
+        const int qi = R.fl[k] >> 8;
+        const size_t f = (size_t)(S.n.f0[qi] + (u - S.n.mptr[qi]));
         if (HARD) {
             if (loop) C.mem_buf[f * 4 + c] = v;
-            else S.v[(i >> 2) * 4 + c] = v;
+            else S.v[mi * 4 + c] = v;
         }
         if (GRAD && late) {
             C.d_edge[f * 2 + j] = de;
-            if (!loop) S.de[(i >> 2) * 2 + j] = de;
+            if (!loop) S.de[mi * 2 + j] = de;
         }
     }
-    if (arc_item) { S.w[ii * 2 + j] = wgt; S.arc[ii] = arc; }
+    for (int i = tid + ITEMS * PASS_TPB; i < T.nm * 4; i += blockDim.x) {   // TK_LOOP tasks
+        const int u = T.m0 + (i >> 2);
+        const int pp = t.tm_pin[u], ff = t.tm_flags[u];
+        double a_r0 = 0, a_rto = 0, a_ado = 0, a_nd = 0, a_at = 0, a_adj0 = 0, a_lse = 0, a_epl = 0,
+               a_dout = 0;
+        bwd_gather<HARD, GRAD>(C, pp, ff, t.tm_o1_to[u], t.tm_o1_arc[u], t.tm_e1[u], c, t, a_r0,
+                               a_rto, a_ado, a_nd, a_at, a_adj0, a_lse, a_epl, a_dout);
+        double v = 0, de = 0;
+        bwd_member<HARD, GRAD>(t, C, u, pp, ff, c, g, kind, a_r0, a_rto, a_ado, a_nd, a_at, a_adj0,
+                               a_lse, a_epl, a_dout, v, de);
+        const size_t f = (size_t)(S.n.f0[0] + (u - S.n.mptr[0]));
+        if (HARD) C.mem_buf[f * 4 + c] = v;
+        if (GRAD && late) C.d_edge[f * 2 + j] = de;
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++)
+        if (R.arc[k] >= 0) {
+            const int ai = ii + k * TASK_Q;
+            S.w[ai * 2 + j] = wgt[k];
+            S.arc[ai] = R.arc[k];
+        }
     __syncthreads();
     if (chunk) {
         // one chunk of a big star net: ordered partial folds, last chunk combines
@@ -705,116 +845,152 @@ __global__ void __launch_bounds__(PASS_TPB) k_bwd(Topo t, Corners cs, int k0, do
                 part[4 + j] = ps;
             }
         }
-        if (!last_chunk(C.big_ctr + 4 * T.slot + variant, nch, &S.flag)) return;
-        if (tid >= 4) return;
-        const int rt = S.n.root[0], fq = S.n.flags[0];
-        const double* p0 = C.big_part + (size_t)t.bn_part0[T.slot] * 8;
+        const bool last = last_chunk(C.big_ctr + 4 * T.slot + variant, nch, &S.flag);
+        if (last && tid < 4) {
+            const int rt = S.n.root[0], fq = S.n.flags[0];
+            const double* p0 = C.big_part + (size_t)t.bn_part0[T.slot] * 8;
+            if (HARD) {
+                const bool mx = c < 2;
+                double rr = root_init_required(t, C, rt, fq, S.n.e1[0], c);
+                for (int k = 0; k < nch; k++)
+                    if (later_wins(mx, rr, LDG(p0 + k * 8 + c))) rr = LDG(p0 + k * 8 + c);
+                C.required[(size_t)rt * 4 + c] = rr;
+                if (!(fq & TQ_ROOT_MEMBER)) {
+                    const double a = LDG(C.arrival + (size_t)rt * 4 + c);
+                    C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
+                }
+            }
+            if (GRAD && late) {
+                double ar = root_seed(t, C, rt, fq, S.n.e1[0], j, g, kind);
+                for (int k = nch - 1; k >= 0; k--) ar = __dadd_rn(ar, LDG(p0 + k * 8 + 4 + j));
+                C.adjoint[(size_t)rt * 2 + j] = ar;
+                if ((fq & TQ_KIND) == ROOT_ARC)
+                    for (int q = 0; q < T.na; q++)
+                        C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
+            }
+        }
+        __syncthreads();
+        return;
+    }
+    // ---- net phase: one (net, cond) per thread
+    if (ii < T.nq) {
+        const int rt = S.n.root[ii], fq = S.n.flags[ii];
+        const int k0m = S.n.mptr[ii] - T.m0, k1m = S.n.mptr[ii + 1] - T.m0;
         if (HARD) {
             const bool mx = c < 2;
-            double rr = (fq & TQ_MULTI_EP) ? init_required_multi(t, C, rt, c)
-                                           : merge_req(c < 2 ? -INF : INF,
-                                                       (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)S.n.e1[0] * 4 + c]
-                                                                         : (c < 2 ? -INF : INF), c);
-            for (int k = 0; k < nch; k++)
-                if (later_wins(mx, rr, p0[k * 8 + c])) rr = p0[k * 8 + c];
+            double rr = root_init_required(t, C, rt, fq, S.n.e1[ii], c);
+            if (loop) {
+                const int s = S.n.f0[ii];
+                for (int k = 0; k < k1m - k0m; k++) {
+                    const double v = LDG(C.mem_buf + (size_t)(s + k) * 4 + c);
+                    if (later_wins(mx, rr, v)) rr = v;
+                }
+            } else {
+                for (int k = k0m; k < k1m; k++)
+                    if (later_wins(mx, rr, S.v[k * 4 + c])) rr = S.v[k * 4 + c];
+            }
             C.required[(size_t)rt * 4 + c] = rr;
             if (!(fq & TQ_ROOT_MEMBER)) {
-                const double a = C.arrival[(size_t)rt * 4 + c];
+                const double a = LDG(C.arrival + (size_t)rt * 4 + c);
                 C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
             }
         }
         if (GRAD && late) {
-            double ar = 0.0;
-            if (fq & TQ_ROOT_EP) {
-                const double l = C.lse_at[(size_t)rt * 2 + j];
-                ar = (fq & TQ_MULTI_EP) ? seed_multi(t, C, rt, j, l, g, kind)
-                                        : __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)S.n.e1[0] * 4 + 2 + j]), g, kind));
-            }
-            for (int k = nch - 1; k >= 0; k--) ar = __dadd_rn(ar, p0[k * 8 + 4 + j]);
-            C.adjoint[(size_t)rt * 2 + j] = ar;
-            if ((fq & TQ_KIND) == ROOT_ARC)
-                for (int q = 0; q < T.na; q++)
-                    C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
-        }
-        return;
-    }
-    // net phase: one (net, cond) per thread
-    if (ii >= T.nq) return;
-    const int rt = S.n.root[ii], fq = S.n.flags[ii];
-    const int k0m = S.n.mptr[ii] - T.m0, k1m = S.n.mptr[ii + 1] - T.m0;
-    if (HARD) {
-        const bool mx = c < 2;
-        double rr = (fq & TQ_MULTI_EP) ? init_required_multi(t, C, rt, c)
-                                       : merge_req(c < 2 ? -INF : INF,
-                                                   (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)S.n.e1[ii] * 4 + c]
-                                                                     : (c < 2 ? -INF : INF), c);
-        if (loop) {
-            const int s = S.n.f0[ii];
-            for (int k = 0; k < k1m - k0m; k++) {
-                const double v = C.mem_buf[(size_t)(s + k) * 4 + c];
-                if (later_wins(mx, rr, v)) rr = v;
-            }
-        } else {
-            for (int k = k0m; k < k1m; k++)
-                if (later_wins(mx, rr, S.v[k * 4 + c])) rr = S.v[k * 4 + c];
-        }
-        C.required[(size_t)rt * 4 + c] = rr;
-        if (!(fq & TQ_ROOT_MEMBER)) {
-            const double a = C.arrival[(size_t)rt * 4 + c];
-            C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
-        }
-    }
-    if (GRAD && late) {
-        double ar = 0.0;
-        if (fq & TQ_ROOT_EP) {
-            const double l = C.lse_at[(size_t)rt * 2 + j];
-            ar = (fq & TQ_MULTI_EP) ? seed_multi(t, C, rt, j, l, g, kind)
-                                    : __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)S.n.e1[ii] * 4 + 2 + j]), g, kind));
-        }
-        if ((fq & TQ_TREE) || loop) {
-            // parents gather children, deepest member first (diff.py:222-233)
-            const int s = S.n.f0[ii];
-            for (int k = k1m - k0m - 1; k >= 0; k--) {
-                const double dk = C.d_edge[(size_t)(s + k) * 2 + j];
-                const int pl = (fq & TQ_TREE) ? t.mem_parent_loc[s + k] : 0;
-                if (pl > 0) {
-                    double* dp = C.d_edge + (size_t)(s + pl - 1) * 2 + j;
-                    *dp = __dadd_rn(*dp, dk);
-                } else {
-                    ar = __dadd_rn(ar, dk);
+            double ar = root_seed(t, C, rt, fq, S.n.e1[ii], j, g, kind);
+            if ((fq & TQ_TREE) || loop) {
+                // parents gather children, deepest member first (diff.py:222-233)
+                const int s = S.n.f0[ii];
+                for (int k = k1m - k0m - 1; k >= 0; k--) {
+                    const double dk = LDG(C.d_edge + (size_t)(s + k) * 2 + j);
+                    const int pl = (fq & TQ_TREE) ? t.mem_parent_loc[s + k] : 0;
+                    if (pl > 0) {
+                        double* dp = C.d_edge + (size_t)(s + pl - 1) * 2 + j;
+                        *dp = __dadd_rn(LDG(dp), dk);
+                    } else {
+                        ar = __dadd_rn(ar, dk);
+                    }
                 }
-            }
-        } else {
-            for (int k = k1m - 1; k >= k0m; k--) ar = __dadd_rn(ar, S.de[k * 2 + j]);
-        }
-        C.adjoint[(size_t)rt * 2 + j] = ar;
-        if ((fq & TQ_KIND) == ROOT_ARC) {
-            if (!wide) {
-                for (int q = S.n.aptr[ii] - T.a0; q < S.n.aptr[ii + 1] - T.a0; q++)
-                    C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
             } else {
-                for (int q = S.n.aptr[0]; q < S.n.aptr[1]; q++) {
-                    const size_t a = (size_t)t.ta_arc[q];
-                    C.d_arc[a * 2 + j] = __dmul_rn(ar, C.weights[a * 2 + j]);
+                for (int k = k1m - 1; k >= k0m; k--) ar = __dadd_rn(ar, S.de[k * 2 + j]);
+            }
+            C.adjoint[(size_t)rt * 2 + j] = ar;
+            if ((fq & TQ_KIND) == ROOT_ARC) {
+                if (!wide) {
+                    for (int q = S.n.aptr[ii] - T.a0; q < S.n.aptr[ii + 1] - T.a0; q++)
+                        C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
+                } else {
+                    for (int q = S.n.aptr[0]; q < S.n.aptr[1]; q++) {
+                        const size_t a = (size_t)t.ta_arc[q];
+                        C.d_arc[a * 2 + j] = __dmul_rn(ar, LDG(C.weights + a * 2 + j));
+                    }
                 }
             }
         }
     }
+    __syncthreads();                         // smem reusable by the next task
+}
+
+// ---- per-level kernels (one task per block; PDL prologue = records) --------
+
+__global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w)
+{
+    __shared__ RcSmem S;
+    pdl_trigger();
+    const Task T = load_task(t, blockIdx.x);
+    RcRec R;
+    rc_records(t, T, S, R);
+    pdl_wait();
+    rc_body(t, cs.c[blockIdx.y], T, S, R, w);
+}
+
+template <bool HARD, bool LSE>
+__global__ void __launch_bounds__(PASS_TPB, 2) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
+                                                     bool use_smem, double g)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ FwdSmem S;
+    pdl_trigger();
+    const Corner& C = cs.c[blockIdx.y];
+    LutView L;
+    if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
+    const Task T = load_task(t, k0 + blockIdx.x);
+    FwdRec R;
+    fwd_records<HARD>(t, T, S, R);
+    pdl_wait();          // the previous level's results are now visible
+    fwd_body<HARD, LSE>(t, L, C, T, S, R, g);
+}
+
+template <bool HARD, bool GRAD>
+__global__ void __launch_bounds__(PASS_TPB, 2) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
+                                                     int variant)
+{
+    __shared__ BwdSmem S;
+    pdl_trigger();
+    const Task T = load_task(t, k0 + blockIdx.x);
+    BwdRec R;
+    bwd_records<GRAD>(t, T, S, R);
+    pdl_wait();          // the next-higher level's results are now visible
+    bwd_body<HARD, GRAD>(t, cs.c[blockIdx.y], T, S, R, g, kind, variant);
 }
 
 // pins finished after the level loop: pins in no net (seed + out-arcs) and
 // PI roots that also source arcs (their level-loop adjoint + out-arcs)
+__device__ void fin_item(const Topo& t, const Corner& C, int i, double g, int kind)
+{
+    const int p = t.fin_pins[i >> 1], j = i & 1;
+    double ad = t.fin_flags[i >> 1] ? LDG(C.adjoint + (size_t)p * 2 + j)
+                                    : seed_multi(t, C, p, j, LDG(C.lse_at + (size_t)p * 2 + j), g, kind);
+    for (int q = t.pin_out_ptr[p]; q < t.pin_out_ptr[p + 1]; q++)
+        ad = __dadd_rn(ad, LDG(C.d_arc + (size_t)t.pin_out_arc[q] * 2 + j));
+    C.adjoint[(size_t)p * 2 + j] = ad;
+}
+
 __global__ void k_fin(Topo t, Corners cs, double g, int kind)
 {
-    const Corner& C = cs.c[blockIdx.y];
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 2 * t.n_fin) return;
-    const int p = t.fin_pins[i >> 1], j = i & 1;
-    double ad = t.fin_flags[i >> 1] ? C.adjoint[(size_t)p * 2 + j]
-                                    : seed_multi(t, C, p, j, C.lse_at[(size_t)p * 2 + j], g, kind);
-    for (int q = t.pin_out_ptr[p]; q < t.pin_out_ptr[p + 1]; q++)
-        ad = __dadd_rn(ad, C.d_arc[(size_t)t.pin_out_arc[q] * 2 + j]);
-    C.adjoint[(size_t)p * 2 + j] = ad;
+    if (i < 2 * t.n_fin) fin_item(t, cs.c[blockIdx.y], i, g, kind);
 }
 
 // slack over every pin from the current arrival / required (WS_RUN_SLACK)
@@ -852,38 +1028,45 @@ __device__ __forceinline__ void summary_terms(const Topo& t, const Corner& C, in
 {
     const int e = i >> 1, j = i & 1;
     const int pin = t.ep_pin[e];
-    slack = C.slack[(size_t)pin * 4 + 2 + j];
+    slack = LDG(C.slack + (size_t)pin * 4 + 2 + j);
     tns_term = (slack <= 0.0 || slack != slack) ? slack : 0.0;      // np.minimum(s, 0.0)
     loss_term = 0.0;
     if (want_loss) {
-        const double v = __dsub_rn(C.lse_at[(size_t)pin * 2 + j], C.ep_required[(size_t)e * 4 + 2 + j]);
+        const double v = __dsub_rn(LDG(C.lse_at + (size_t)pin * 2 + j), C.ep_required[(size_t)e * 4 + 2 + j]);
         const double mxv = (v >= 0.0 || v != v) ? v : 0.0;           // np.maximum(v, 0.0)
         if (kind == 0) loss_term = mxv;
         else loss_term = __dadd_rn(mxv, __dmul_rn(g, log1p(exp(__ddiv_rn(-fabs(v), g)))));
     }
 }
 
-__global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, const int* leaf_off,
-                                                 const int* leaf_len, int n_leaves,
-                                                 const int* in_left, const int* in_right,
-                                                 const int* height_ptr, int n_heights, double g,
-                                                 int kind, bool want_loss, bool want_sta)
+struct SumArgs {
+    const int *leaf_off, *leaf_len;
+    int n_leaves;
+    const int *in_left, *in_right, *height_ptr;
+    int n_heights;
+};
+
+struct SumSmem {
+    double t[8][128], l[8][128];
+    int last;
+};
+
+// leaves strided over the warps of `ncta` blocks; the last block to finish
+// combines the tree (sync_ctr[0] counts finished blocks)
+__device__ void summary_phase(const Topo& t, const Corner& C, const SumArgs& P, double g, int kind,
+                              bool want_loss, bool want_sta, int cta, int ncta, SumSmem& S)
 {
-    const Corner& C = cs.c[blockIdx.y];
-    __shared__ double s_t[8][128], s_l[8][128];
-    __shared__ bool s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lf = blockIdx.x * 8 + warp;
     double* nv = C.red_tmp;   // [3 * nodes]: tns, loss, wns per node
-    const int nn = 2 * n_leaves - 1;
-    if (lf < n_leaves) {
-        const int off = leaf_off[lf], n = leaf_len[lf];
+    const int nn = 2 * P.n_leaves - 1;
+    for (int lf = cta * 8 + warp; lf < P.n_leaves; lf += ncta * 8) {
+        const int off = P.leaf_off[lf], n = P.leaf_len[lf];
         double wmin = INF;
         for (int k = lane; k < n; k += 32) {
             double tt, sl, lt;
             summary_terms(t, C, off + k, g, kind, want_loss, tt, sl, lt);
-            s_t[warp][k] = tt;
-            s_l[warp][k] = lt;
+            S.t[warp][k] = tt;
+            S.l[warp][k] = lt;
             wmin = (sl < wmin || sl != sl) ? sl : wmin;
         }
         for (int o = 16; o > 0; o >>= 1) {
@@ -894,11 +1077,11 @@ __global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, const int* 
         // lanes 0..7 own accumulator j of numpy's unrolled pairwise leaf
         double rt = 0.0, rl = 0.0;
         if (n >= 8 && lane < 8) {
-            rt = s_t[warp][lane];
-            rl = s_l[warp][lane];
+            rt = S.t[warp][lane];
+            rl = S.l[warp][lane];
             for (int i = 8; i < n - (n % 8); i += 8) {
-                rt = __dadd_rn(rt, s_t[warp][i + lane]);
-                rl = __dadd_rn(rl, s_l[warp][i + lane]);
+                rt = __dadd_rn(rt, S.t[warp][i + lane]);
+                rl = __dadd_rn(rl, S.l[warp][i + lane]);
             }
         }
         double r8t[8], r8l[8];
@@ -920,30 +1103,31 @@ __global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, const int* 
                 i = n - (n % 8);
             }
             for (; i < n; i++) {
-                ts = __dadd_rn(ts, s_t[warp][i]);
-                ls = __dadd_rn(ls, s_l[warp][i]);
+                ts = __dadd_rn(ts, S.t[warp][i]);
+                ls = __dadd_rn(ls, S.l[warp][i]);
             }
             nv[lf] = ts;
             nv[nn + lf] = ls;
             nv[2 * nn + lf] = wmin;
         }
+        __syncwarp();
     }
     // the last block to finish combines the tree
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(C.sync_ctr, 1u);
-        s_last = prev == gridDim.x - 1;
+        S.last = prev == (unsigned)(ncta - 1);
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!S.last) return;
     __threadfence();
-    for (int h = 0; h < n_heights; h++) {
-        for (int k = height_ptr[h] + threadIdx.x; k < height_ptr[h + 1]; k += blockDim.x) {
-            const int l = in_left[k], r = in_right[k], me = n_leaves + k;
-            nv[me] = __dadd_rn(nv[l], nv[r]);
-            nv[nn + me] = __dadd_rn(nv[nn + l], nv[nn + r]);
-            const double a = nv[2 * nn + l], b = nv[2 * nn + r];
+    for (int h = 0; h < P.n_heights; h++) {
+        for (int k = P.height_ptr[h] + threadIdx.x; k < P.height_ptr[h + 1]; k += blockDim.x) {
+            const int l = P.in_left[k], r = P.in_right[k], me = P.n_leaves + k;
+            nv[me] = __dadd_rn(LDG(nv + l), LDG(nv + r));
+            nv[nn + me] = __dadd_rn(LDG(nv + nn + l), LDG(nv + nn + r));
+            const double a = LDG(nv + 2 * nn + l), b = LDG(nv + 2 * nn + r);
             nv[2 * nn + me] = (b < a || b != b) ? b : a;
         }
         __threadfence_block();
@@ -955,6 +1139,15 @@ __global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, const int* 
         if (want_loss) C.summary[2] = nv[nn + top];
         *C.sync_ctr = 0u;
     }
+}
+
+__global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, SumArgs P, double g, int kind,
+                                                 bool want_loss, bool want_sta)
+{
+    __shared__ SumSmem S;
+    pdl_trigger();
+    pdl_wait();
+    summary_phase(t, cs.c[blockIdx.y], P, g, kind, want_loss, want_sta, blockIdx.x, gridDim.x, S);
 }
 
 __global__ void k_summary_empty(Corners cs, bool want_loss, bool want_sta)
@@ -1009,6 +1202,131 @@ __global__ void k_perturb(int M, int N, Corner D, Corner S, unsigned long long s
         const int n = i - M;
         const double f = perturb_factor(seed, 2ull * M + n, sigma);
         for (int c = 0; c < 4; c++) D.root_cap[(size_t)n * 4 + c] = S.root_cap[(size_t)n * 4 + c] * f;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent pass: ONE cooperative launch runs the whole differentiable pass.
+// Every block stages the LUT pool once, then walks RC, the forward levels and
+// the backward levels; blocks of a corner meet at a grid barrier between
+// levels.  Before each barrier a block already loads the records of its
+// first task of the next level (static topology), so after the barrier only
+// the gathers of the just-finished level remain on the critical path.
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// sense-free generation barrier over the `n` blocks of one corner; all of
+// them are co-resident (cooperative launch).  The gpu-scope fences order
+// each block's writes before the barrier and (CCTL.IVALL) drop stale L1 lines.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned n)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == n - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (ld_acquire(bar + 1) == gen) { }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+union PassSmem {
+    RcSmem r;
+    FwdSmem f;
+    BwdSmem b;
+    SumSmem s;
+};
+
+template <bool LSE, bool GRAD>
+__global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners cs, SumArgs P,
+                                                      int w, double g, int kind, bool use_smem)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ PassSmem S;
+    const Corner& C = cs.c[blockIdx.y];
+    unsigned* bar = C.sync_ctr + 1;
+    const int cta = blockIdx.x, ncta = gridDim.x;
+    const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
+    // ---- pins in no net, RC of every net
+    for (int i = cta * PASS_TPB + threadIdx.x; i < t.n_free; i += ncta * PASS_TPB)
+        free_pin(t, C, i, LSE);
+    for (int k = cta; k < t.n_tasks; k += ncta) {
+        const Task T = load_task(t, k);
+        RcRec R;
+        rc_records(t, T, S.r, R);
+        rc_body(t, C, T, S.r, R, w);
+    }
+    // ---- forward levels
+    {
+        int k = t.lvt_ptr[0] + cta;
+        bool have = t.L > 0 && k < t.lvt_ptr[1];
+        Task T{};
+        FwdRec R;
+        if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
+        grid_sync(bar, ncta);
+        for (int li = 0; li < t.L; li++) {
+            const int kend = t.lvt_ptr[li + 1];
+            while (have) {
+                fwd_body<true, LSE>(t, L, C, T, S.f, R, g);
+                k += ncta;
+                have = k < kend;
+                if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
+            }
+            if (li + 1 < t.L) {
+                k = t.lvt_ptr[li + 1] + cta;
+                have = k < t.lvt_ptr[li + 2];
+                if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
+            }
+            grid_sync(bar, ncta);
+        }
+    }
+    // ---- backward levels
+    {
+        const int variant = GRAD ? 3 : 1;
+        int li = t.L - 1;
+        int k = li >= 0 ? t.lvt_ptr[li] + cta : 0;
+        bool have = li >= 0 && k < t.lvt_ptr[li + 1];
+        Task T{};
+        BwdRec R;
+        if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+        for (; li >= 0; li--) {
+            const int kend = t.lvt_ptr[li + 1];
+            while (have) {
+                bwd_body<true, GRAD>(t, C, T, S.b, R, g, kind, variant);
+                k += ncta;
+                have = k < kend;
+                if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+            }
+            if (li > 0) {
+                k = t.lvt_ptr[li - 1] + cta;
+                have = k < t.lvt_ptr[li];
+                if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+            }
+            grid_sync(bar, ncta);
+        }
+    }
+    // ---- pins finished after the level loop, then TNS / WNS / loss
+    if (GRAD)
+        for (int i = cta * PASS_TPB + threadIdx.x; i < 2 * t.n_fin; i += ncta * PASS_TPB)
+            fin_item(t, C, i, g, kind);
+    if (P.n_leaves > 0) {
+        summary_phase(t, C, P, g, kind, GRAD, true, cta, ncta, S.s);
+    } else if (cta == 0 && threadIdx.x == 0) {
+        C.summary[0] = 0.0;
+        C.summary[1] = INF;
+        if (GRAD) C.summary[2] = 0.0;
     }
 }
 
@@ -1082,6 +1400,25 @@ void launch_perturb(const Context& ctx, int dst, int src, unsigned long long see
 
 namespace {
 
+// every pass kernel is launched with programmatic stream serialization so
+// its static prologue overlaps the previous kernel (see pdl_wait)
+template <typename... KArgs, typename... Args>
+void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+            Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    WS_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 struct Launcher {
     Context& ctx;
     Corners cs;
@@ -1095,7 +1432,7 @@ struct Launcher {
         for (int k = 0; k < nc; k++) cs.c[k] = ctx.corners[c0 + k].d;
         const Topo& t = ctx.t;
         ls = {t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, t.NL,
-              ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len};
+              ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len, t.lut_info};
         lut_bytes = lut_smem_bytes(t.NL, ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len);
         use_smem = lut_bytes <= 96 * 1024;
         if (!use_smem) lut_bytes = 0;
@@ -1106,22 +1443,30 @@ struct Launcher {
     void free_pins(cudaStream_t s, bool lse)
     {
         if (!ctx.t.n_free) return;
-        k_free<<<grid1(ctx.t.n_free, 256), 256, 0, s>>>(ctx.t, cs, lse);
+        launch(k_free, grid1(ctx.t.n_free, 256), dim3(256), 0, s, ctx.t, cs, lse);
         count++;
     }
     void rc(cudaStream_t s, int w)
     {
         if (!ctx.t.n_tasks) return;
-        k_rc<<<dim3(ctx.t.n_tasks, nc), PASS_TPB, 0, s>>>(ctx.t, cs, w);
+        launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
         count++;
+    }
+    // WS_PROBE builds: launch i stamps into probe + i * PROBE_STRIDE
+    static constexpr size_t PROBE_STRIDE = 8 * 2048;
+    Topo probed(int nt) const
+    {
+        Topo tt = ctx.t;
+        tt.probe = (ctx.t.probe && nt <= 2048) ? ctx.t.probe + (size_t)count * PROBE_STRIDE : nullptr;
+        return tt;
     }
     template <bool H, bool Lse>
     void fwd(cudaStream_t s, int li, double g)
     {
         const int nt = tasks(li);
         if (nt <= 0) return;
-        k_fwd<H, Lse><<<dim3(nt, nc), PASS_TPB, H ? lut_bytes : 0, s>>>(
-            ctx.t, ls, cs, ctx.lvt_ptr_host[li], use_smem, g);
+        launch(k_fwd<H, Lse>, dim3(nt, nc), dim3(PASS_TPB), H ? lut_bytes : 0, s, probed(nt), ls, cs,
+               ctx.lvt_ptr_host[li], use_smem, g);
         count++;
     }
     template <bool H, bool G>
@@ -1130,14 +1475,14 @@ struct Launcher {
         const int nt = tasks(li);
         if (nt <= 0) return;
         const int variant = H && G ? 3 : (H ? 1 : 2);
-        k_bwd<H, G><<<dim3(nt, nc), PASS_TPB, 0, s>>>(ctx.t, cs, ctx.lvt_ptr_host[li], g, kind,
-                                                      variant);
+        launch(k_bwd<H, G>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs, ctx.lvt_ptr_host[li],
+               g, kind, variant);
         count++;
     }
     void fin(cudaStream_t s, double g, int kind)
     {
         if (!ctx.t.n_fin) return;
-        k_fin<<<grid1(2 * ctx.t.n_fin, 256), 256, 0, s>>>(ctx.t, cs, g, kind);
+        launch(k_fin, grid1(2 * ctx.t.n_fin, 256), dim3(256), 0, s, ctx.t, cs, g, kind);
         count++;
     }
     void slack_all(cudaStream_t s)
@@ -1152,6 +1497,41 @@ struct Launcher {
         k_lse_seed<<<grid1(ctx.t.P, 256), 256, 0, s>>>(ctx.t, cs);
         count++;
     }
+    SumArgs sum_args() const
+    {
+        const SumPlan* pl = ctx.tns_plan;
+        return SumArgs{pl->leaf_off, pl->leaf_len, pl->n_leaves, pl->in_left, pl->in_right,
+                       pl->d_height_ptr, (int)pl->height_ptr.size() - 1};
+    }
+    // the whole pass as one cooperative kernel
+    template <bool Lse, bool G>
+    void persistent(cudaStream_t s, int w, double g, int kind)
+    {
+        auto kern = k_pass<Lse, G>;
+        if (lut_bytes > 48 * 1024)
+            WS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_bytes));
+        int per_sm = 0, dev = 0, n_sm = 0;
+        WS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PASS_TPB, lut_bytes));
+        WS_CUDA(cudaGetDevice(&dev));
+        WS_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        int max_tasks = 1;
+        for (int li = 0; li < ctx.t.L; li++) max_tasks = std::max(max_tasks, tasks(li));
+        const int cap = per_sm * n_sm / nc;
+        if (cap < 1) throw Error(WS_ERR_VALUE, "persistent pass: too many corners for one launch");
+        const int ncta = std::min(cap, std::max(max_tasks, std::min(ctx.t.n_tasks, cap)));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ncta, nc);
+        cfg.blockDim = dim3(PASS_TPB);
+        cfg.dynamicSmemBytes = lut_bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        WS_CUDA(cudaLaunchKernelEx(&cfg, kern, ctx.t, ls, cs, sum_args(), w, g, kind, use_smem));
+        count++;
+    }
     void summary(cudaStream_t s, double g, int kind, bool want_loss, bool want_sta)
     {
         const SumPlan* pl = ctx.tns_plan;
@@ -1160,9 +1540,8 @@ struct Launcher {
             count++;
             return;
         }
-        k_summary<<<dim3((pl->n_leaves + 7) / 8, nc), 256, 0, s>>>(
-            ctx.t, cs, pl->leaf_off, pl->leaf_len, pl->n_leaves, pl->in_left, pl->in_right,
-            pl->d_height_ptr, (int)pl->height_ptr.size() - 1, g, kind, want_loss, want_sta);
+        launch(k_summary, dim3((pl->n_leaves + 7) / 8, nc), dim3(256), 0, s, ctx.t, cs, sum_args(),
+               g, kind, want_loss, want_sta);
         count++;
     }
 };
@@ -1180,7 +1559,10 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
     const bool fused = (flags & WS_RUN_FUSED) && hard && lse && grad;
     const bool two = (flags & WS_RUN_TWO_STREAM) && hard && (lse || grad) && !fused;
 
-    if (fused) {
+    if ((flags & WS_RUN_PERSISTENT) && hard && ((lse && grad) || (!lse && !grad))) {
+        if (lse) la.persistent<true, true>(s, w, g, kind);
+        else la.persistent<false, false>(s, w, g, kind);
+    } else if (fused) {
         la.free_pins(s, true);
         la.rc(s, w);
         for (int li = 0; li < L; li++) la.fwd<true, true>(s, li, g);

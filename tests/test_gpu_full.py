@@ -63,12 +63,13 @@ def test_full_size_parity(cfg_name):
     for f in G_FIELDS:
         assert grad_close(dev.get(f), getattr(og, f)), (f, max_rel(dev.get(f), getattr(og, f)))
     assert loss == pytest.approx(og.loss, rel=1e-9)
-    # two-stream mode is bitwise identical to the fused single stream
+    # two-stream and persistent modes are bitwise identical to the fused single stream
     ref = {f: dev.get(f) for f in ST_FIELDS + G_FIELDS}
-    dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_TWO_STREAM)
-    for f in ST_FIELDS + G_FIELDS:
-        assert np.array_equal(dev.get(f), ref[f]), f
-    assert dev.summary()[2] == loss
+    for extra in (_lib.RUN_TWO_STREAM, _lib.RUN_PERSISTENT):
+        dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | extra)
+        for f in ST_FIELDS + G_FIELDS:
+            assert np.array_equal(dev.get(f), ref[f]), (extra, f)
+        assert dev.summary()[2] == loss
     dev.close()
 
 

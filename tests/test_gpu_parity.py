@@ -199,6 +199,28 @@ def test_chain_kats():
     assert np.array_equal(gl.lse_arrival, ws.run_engine(flat).arrival[:, 2:4])
 
 
+@pytest.mark.parametrize("name", CASES)
+def test_persistent_pass_bit_identical(name):
+    """One cooperative kernel for the whole pass == the per-level kernels."""
+    from paper_2603_28381_b200 import _lib
+    flat = flat_of(name)
+    dev = flat.dev
+    ws.run_engine(flat)   # uploads the flat's values
+    base = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
+    dev.run(base | _lib.RUN_FUSED)
+    ref = {f: dev.get(f) for f in ST_FIELDS + G_FIELDS}
+    ref_sum = dev.summary()
+    for flags in (base | _lib.RUN_PERSISTENT, base | _lib.RUN_PERSISTENT | _lib.RUN_GRAPH):
+        dev.run(flags)
+        for f in ST_FIELDS + G_FIELDS:
+            assert np.array_equal(dev.get(f), ref[f]), (flags, f)
+        assert dev.summary() == ref_sum
+    dev.run(_lib.RUN_HARD | _lib.RUN_PERSISTENT)
+    for f in ST_FIELDS:
+        assert np.array_equal(dev.get(f), ref[f]), f
+    assert dev.summary()[:2] == ref_sum[:2]
+
+
 def test_graph_replay_bit_identical():
     g = load("gen_c1_star")
     flat = flat_of("gen_c1_star")
