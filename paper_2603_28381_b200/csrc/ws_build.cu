@@ -383,6 +383,17 @@ int reduce_max(Scratch& sc, Arena& ar, const int* a, int n, cudaStream_t s)
     return h;
 }
 
+// streaming-RC member code: -1 for members of tree nets (handled per net),
+// else pin << 1 | (pin roots a net: its load comes from that net)
+__global__ void k_rc_code(int M, const int* mem_pin, const int* mem_net, const int* net_tree,
+                          const int* root_net_of_pin, int* code)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= M) return;
+    const int pin = mem_pin[f];
+    code[f] = net_tree[mem_net[f]] ? -1 : (pin << 1) | (root_net_of_pin[pin] >= 0 ? 1 : 0);
+}
+
 }  // namespace
 
 
@@ -800,6 +811,12 @@ void build_topology(Context& ctx, const ws_design_desc* d)
     }
     t.max_in = reduce_max(sc, ar, t.net_a, N, s);
     t.max_m = reduce_max(sc, ar, t.net_m, N, s);
+    t.rc_code = ar.alloc<int>(M);
+    if (M) {
+        k_rc_code<<<blocks_for(M), TPB, 0, s>>>(M, t.mem_pin, t.mem_net, t.net_tree,
+                                                  t.root_net_of_pin, t.rc_code);
+        WS_CHECK_LAUNCH();
+    }
 
     // host copies of the level schedule and per-level shape stats
     ctx.lv_ptr_host.assign(t.L + 1, 0);

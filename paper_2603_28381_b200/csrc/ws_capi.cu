@@ -1,5 +1,6 @@
 // C ABI (include/warpstar.h): context lifetime, value upload, pass launch,
 // result download, and the legacy per-level shims.
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -206,6 +207,10 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
         h = new ws_ctx();
         ws::Context& c = h->c;
         c.clock_period = d->clock_period;
+        {
+            const char* e = getenv("WS_LUT_GLOBAL");
+            c.lut_global = e && e[0] == '1';
+        }
         WS_CUDA(cudaStreamCreateWithFlags(&c.s_main, cudaStreamNonBlocking));
         WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamNonBlocking));
         ws::build_topology(c, d);

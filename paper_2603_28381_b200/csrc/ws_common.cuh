@@ -48,6 +48,7 @@ struct Topo {
     int *level_of, *lv_ptr, *lv_nets;
     // derived work lists
     int *net_tree;                   // 1 if any member has a non-root parent
+    int *rc_code;                    // per member: -1 (tree net) or pin << 1 | (pin is a root)
     int *pin_ep_ptr, *pin_ep_idx;    // endpoint entries grouped by pin (stable)
     int *pin_pi;                     // pin -> PI index or -1
     int *pin_out_ptr, *pin_out_arc;  // arcs grouped by source pin (all pins)
@@ -186,10 +187,20 @@ __device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
 {
     Loc r;
     if (n > 1) {
-        int lo = 0, hi = n;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (ax[mid] <= q) lo = mid + 1; else hi = mid;
+        int lo;
+        if (n <= 8) {
+            // upper_bound on a sorted axis = number of entries <= q: a fixed,
+            // branch-free count instead of the data-dependent search loop
+            lo = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) lo += (k < n && ax[k] <= q) ? 1 : 0;
+        } else {
+            int hi = n;
+            lo = 0;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (ax[mid] <= q) lo = mid + 1; else hi = mid;
+            }
         }
         int i = lo - 1;
         if (i < 0) i = 0; else if (i > n - 2) i = n - 2;

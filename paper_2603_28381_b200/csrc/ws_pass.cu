@@ -284,6 +284,21 @@ __device__ __forceinline__ bool last_chunk(unsigned* ctr, int nch, int* s_flag)
 
 #define LDG(p) __ldcg(p)
 
+// WS_PROBE builds: phase stamps inside task bodies of the persistent kernel
+// (plev >= 0), laid out after the per-level stamps
+#ifdef WS_PROBE
+#define BSTAMP(slot)                                                                          \
+    do {                                                                                      \
+        if (plev >= 0 && threadIdx.x == 0 && t.probe) {                                       \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[(size_t)2 * t.L * 2048 * 4 + ((size_t)plev * 2048 + blockIdx.x) * 4 + (slot)] = _v; \
+        }                                                                                     \
+    } while (0)
+#else
+#define BSTAMP(slot) do { (void)plev; } while (0)
+#endif
+
 // ---- RC --------------------------------------------------------------------
 
 struct RcSmem {
@@ -385,12 +400,18 @@ struct FwdSmem {
     double cm[TASK_Q * 2];      // LSE max per (net, late col)
     double ss[TASK_Q * 2];      // LSE denominator
     double at[TASK_Q * 4], sl[TASK_Q * 4], lr[TASK_Q * 2];   // root results
+    double lf[TASK_Q * 4];      // load-axis locate of the root load (per net, cond) ...
+    int li[TASK_Q * 4];         // ... index, and the canonical axis it was taken on
+    int lax[TASK_Q * 4];
 };
 
 struct FwdRec {
     int from[ITEMS], root[ITEMS], arc[ITEMS], aq[ITEMS];
     unsigned short dl[ITEMS], sl[ITEMS];
     int mpin[ITEMS], mfl[ITEMS];
+    int nroot, nflags, nlut;    // this lane's (net, cond) item: root, flags, first arc's delay LUT
+    // pass-static gathers (RC outputs), prefetched by the persistent kernel
+    double ld[ITEMS], mnd[ITEMS], mim[ITEMS];
 };
 
 // numpy's np.add.reduceat segment: z_0 + pairwise_sum(z_1 .. z_{n-1})
@@ -414,11 +435,61 @@ __device__ __forceinline__ double reduceat_sum(const double* z, int stride, int 
 }
 
 template <bool HARD>
+__device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R);
+
+// the (net, cond) item's root load located on its first arc's load axis
+__device__ __forceinline__ void net_load_locate(const Topo& t, const Corner& C, const FwdRec& R,
+                                                FwdSmem& S, int ii, int c)
+{
+    if (R.nroot < 0 || (R.nflags & TQ_KIND) != ROOT_ARC) return;
+    if (R.nlut >= 0) {
+        const int4 inf = t.lut_info[R.nlut];
+        const Loc lc = lut_locate(t.lut_l_flat + inf.z, inf.w, LDG(C.load + (size_t)R.nroot * 4 + c));
+        S.lf[ii * 4 + c] = lc.f;
+        S.li[ii * 4 + c] = lc.i0 | (lc.i1 << 16);
+        S.lax[ii * 4 + c] = inf.z | (inf.w << 24);
+    } else {
+        S.lax[ii * 4 + c] = -1;
+    }
+}
+
+// persistent kernel: records plus every gather that is static for the whole
+// forward sweep (RC outputs) and the root-load locate
+template <bool HARD>
+__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, const Task& T,
+                                                   FwdSmem& S, FwdRec& R)
+{
+    fwd_records<HARD>(t, T, S, R);
+    const int c = threadIdx.x & 3;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        if (HARD && R.arc[k] >= 0) R.ld[k] = LDG(C.load + (size_t)R.root[k] * 4 + c);
+        if (R.mpin[k] >= 0) {
+            R.mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
+            if (HARD) R.mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
+        }
+    }
+    if (HARD) net_load_locate(t, C, R, S, threadIdx.x >> 2, c);
+}
+
+template <bool HARD>
 __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R)
 {
     load_nets(t, T, S.n);
     const int c = threadIdx.x & 3;
     const bool wide = T.flags & TK_WIDE;
+    R.nroot = -1;
+    {
+        const int qi = threadIdx.x >> 2;
+        if (qi < T.nq) {
+            const int q = T.q0 + qi;
+            R.nroot = t.tq_root[q];
+            R.nflags = t.tq_flags[q];
+            R.nlut = -1;
+            if (HARD && (R.nflags & TQ_KIND) == ROOT_ARC && !wide)
+                R.nlut = lut_c(t.ta_lut[2 * (size_t)t.tq_aptr[q]], c);
+        }
+    }
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
         const int ii = (threadIdx.x >> 2) + k * TASK_Q;
@@ -442,9 +513,9 @@ __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSme
     }
 }
 
-template <bool HARD, bool LSE>
+template <bool HARD, bool LSE, bool STATIC = false>
 __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const Task& T,
-                         FwdSmem& S, const FwdRec& R, double g)
+                         FwdSmem& S, const FwdRec& R, double g, int plev = -1)
 {
     const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
     const bool late = c >= 2;
@@ -459,18 +530,43 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
             if (HARD) {
                 slf[k] = LDG(C.slew + (size_t)R.from[k] * 4 + c);
                 atf[k] = LDG(C.arrival + (size_t)R.from[k] * 4 + c);
-                ld[k] = LDG(C.load + (size_t)R.root[k] * 4 + c);
+                ld[k] = STATIC ? R.ld[k] : LDG(C.load + (size_t)R.root[k] * 4 + c);
             } else {
                 dd[k] = LDG(C.arc_delay + (size_t)R.arc[k] * 4 + c);
             }
             if (LSE && late) xl[k] = LDG(C.lse_at + (size_t)R.from[k] * 2 + j);
         }
         if (R.mpin[k] >= 0) {
-            mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
-            if (HARD) mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
+            if (STATIC) {
+                mnd[k] = R.mnd[k];
+                if (HARD) mim[k] = R.mim[k];
+            } else {
+                mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
+                if (HARD) mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
+            }
+        }
+    }
+    // (net, cond) item: the root's load located once for all its arcs (on the
+    // first arc's delay-LUT load axis), and the seeds of non-arc-driven roots
+    double n_at = 0, n_sl = 0, n_lr = 0;
+    if (R.nroot >= 0) {
+        const int kind = R.nflags & TQ_KIND;
+        if (kind == ROOT_ARC) {
+            if (HARD && !STATIC) net_load_locate(t, C, R, S, ii, c);
+        } else if (kind == ROOT_FEED) {
+            if (HARD) {
+                n_at = LDG(C.arrival + (size_t)R.nroot * 4 + c);
+                n_sl = LDG(C.slew + (size_t)R.nroot * 4 + c);
+            }
+            if (LSE && late) n_lr = LDG(C.lse_at + (size_t)R.nroot * 2 + j);
+        } else if (R.nflags & TQ_ROOT_PI) {
+            const int pi = t.pin_pi[R.nroot];
+            n_at = C.pi_arrival[(size_t)pi * 4 + c];
+            n_sl = C.pi_slew[(size_t)pi * 4 + c];
         }
     }
     __syncthreads();                  // net records (and the LUT pool) visible
+    BSTAMP(0);
     // ---- arc phase: delay LUT, candidate, speculative output slew, LSE operand
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
@@ -481,7 +577,16 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
             // search serves both when their axes coincide
             const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
             const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
-            const Loc lld = lut_locate(L.l + di.z, di.w, ld[k]);
+            Loc lld;
+            const int nax = S.lax[R.aq[k] * 4 + c];
+            if (nax == (di.z | (di.w << 24))) {     // the net-level locate applies
+                const int pk = S.li[R.aq[k] * 4 + c];
+                lld.i0 = pk & 0xffff;
+                lld.i1 = pk >> 16;
+                lld.f = S.lf[R.aq[k] * 4 + c];
+            } else {
+                lld = lut_locate(L.l + di.z, di.w, ld[k]);
+            }
             dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
             const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
             const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld[k]);
@@ -503,6 +608,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
         }
     }
     __syncthreads();
+    BSTAMP(1);
     // ---- net phase 1: merge in arc order (first arc wins ties), LSE max
     const bool first = !(T.flags & TK_CHUNK) || T.m0 == S.n.mptr[0];
     int kind = 0, a0 = 0, a1 = 0, rt = 0;
@@ -559,18 +665,13 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
             }
         } else if (kind == ROOT_FEED) {
             // driven by its parent net's member update (a lower level)
-            if (HARD) {
-                at = LDG(C.arrival + (size_t)rt * 4 + c);
-                sl = LDG(C.slew + (size_t)rt * 4 + c);
-            }
-            if (LSE && late) S.lr[ii * 2 + j] = LDG(C.lse_at + (size_t)rt * 2 + j);
+            at = n_at;
+            sl = n_sl;
+            if (LSE && late) S.lr[ii * 2 + j] = n_lr;
         } else {
             // primary-input root (or undriven): the seeded values
-            if (fl & TQ_ROOT_PI) {
-                const int pi = t.pin_pi[rt];
-                at = C.pi_arrival[(size_t)pi * 4 + c];
-                sl = C.pi_slew[(size_t)pi * 4 + c];
-            }
+            at = n_at;
+            sl = n_sl;
             if (first) {
                 if (HARD) {
                     C.arrival[(size_t)rt * 4 + c] = at;
@@ -603,6 +704,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
         }
     }
     __syncthreads();
+    BSTAMP(2);
     // ---- arc phase 3: softmax weights (alongside the member phase)
     if (LSE && !wide && first && late)
 #pragma unroll
@@ -653,7 +755,11 @@ struct BwdSmem {
 };
 
 struct BwdRec {
-    int pin[ITEMS], fl[ITEMS], o1t[ITEMS], o1a[ITEMS], e1[ITEMS], arc[ITEMS];
+    int pin[ITEMS], fl[ITEMS], o1t[ITEMS], o1a[ITEMS], e1[ITEMS], arc[ITEMS], no[ITEMS], o0[ITEMS];
+    int nroot, nflags, ne1;     // this lane's (net, cond) item
+    // pass-static gathers (forward outputs), prefetched by the persistent kernel
+    double ado[ITEMS], nd[ITEMS], at[ITEMS], lse[ITEMS], epl[ITEMS], wgt[ITEMS], r0[ITEMS];
+    double n_at, n_rr, n_seed;
 };
 
 template <bool GRAD>
@@ -672,21 +778,30 @@ __device__ __forceinline__ void bwd_records(const Topo& t, const Task& T, BwdSme
             R.o1t[k] = t.tm_o1_to[u];
             R.o1a[k] = t.tm_o1_arc[u];
             R.e1[k] = t.tm_e1[u];
+            R.o0[k] = t.tm_optr[u];
+            R.no[k] = t.tm_optr[u + 1] - R.o0[k];
         }
         R.arc[k] = -1;
         if (GRAD && late && ii < T.na && !(T.flags & TK_WIDE)) R.arc[k] = t.ta_arc[T.a0 + ii];
+    }
+    R.nroot = -1;
+    const int qi = threadIdx.x >> 2;
+    if (qi < T.nq) {
+        const int q = T.q0 + qi;
+        R.nroot = t.tq_root[q];
+        R.nflags = t.tq_flags[q];
+        R.ne1 = t.tq_e1[q];
     }
 }
 
 // one member (u, c): fold required over out-arcs, slack, adjoint.
 template <bool HARD, bool GRAD>
-__device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int u, int pin, int fl,
-                                           int c, double g, int kind, double r0, double rto,
+__device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int o0, int o1, int pin,
+                                           int fl, int c, double g, int kind, double r0, double rto,
                                            double ado, double nd, double at, double adj0,
                                            double lse, double epl, double dout, double& v,
                                            double& de)
 {
-    const int o0 = t.tm_optr[u], o1 = t.tm_optr[u + 1];
     if (HARD) {
         const bool mx = c < 2;
         double r = r0;
@@ -765,9 +880,50 @@ __device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int 
     return __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)e1 * 4 + 2 + j]), g, kind));
 }
 
+// persistent kernel: records plus the gathers that are static for the whole
+// backward sweep (forward outputs, endpoint seeds)
 template <bool HARD, bool GRAD>
+__device__ __forceinline__ void bwd_records_static(const Topo& t, const Corner& C, const Task& T,
+                                                   BwdSmem& S, BwdRec& R, double g, int kind)
+{
+    bwd_records<GRAD>(t, T, S, R);
+    const int c = threadIdx.x & 3, j = c - 2;
+    const bool late = c >= 2;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        R.ado[k] = R.nd[k] = R.at[k] = R.lse[k] = R.epl[k] = R.wgt[k] = R.r0[k] = 0.0;
+        if (R.pin[k] >= 0) {
+            const int pin = R.pin[k], fl = R.fl[k];
+            if (HARD) {
+                if (R.o1a[k] >= 0) R.ado[k] = LDG(C.arc_delay + (size_t)R.o1a[k] * 4 + c);
+                R.nd[k] = LDG(C.net_delay + (size_t)pin * 4 + c);
+                R.at[k] = LDG(C.arrival + (size_t)pin * 4 + c);
+                if (!(fl & TM_ROOT))
+                    R.r0[k] = (fl & TM_MULTI_EP) ? init_required_multi(t, C, pin, c)
+                                                 : merge_req(c < 2 ? -INF : INF,
+                                                             (fl & TM_EP) ? C.ep_required[(size_t)R.e1[k] * 4 + c]
+                                                                          : (c < 2 ? -INF : INF), c);
+            }
+            if (GRAD && late && (fl & TM_EP)) {
+                R.lse[k] = LDG(C.lse_at + (size_t)pin * 2 + j);
+                R.epl[k] = C.ep_required[(size_t)R.e1[k] * 4 + 2 + j];
+            }
+        }
+        if (R.arc[k] >= 0) R.wgt[k] = LDG(C.weights + (size_t)R.arc[k] * 2 + j);
+    }
+    R.n_at = R.n_rr = R.n_seed = 0.0;
+    if (R.nroot >= 0) {
+        if (HARD) {
+            if (!(R.nflags & TQ_ROOT_MEMBER)) R.n_at = LDG(C.arrival + (size_t)R.nroot * 4 + c);
+            R.n_rr = root_init_required(t, C, R.nroot, R.nflags, R.ne1, c);
+        }
+        if (GRAD && late) R.n_seed = root_seed(t, C, R.nroot, R.nflags, R.ne1, j, g, kind);
+    }
+}
+
+template <bool HARD, bool GRAD, bool STATIC = false>
 __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem& S,
-                         const BwdRec& R, double g, int kind, int variant)
+                         const BwdRec& R, double g, int kind, int variant, int plev = -1)
 {
     const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
     const bool late = c >= 2;
@@ -779,20 +935,49 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
         r0[k] = rto[k] = ado[k] = nd[k] = at[k] = adj0[k] = lse[k] = epl[k] = dout[k] = wgt[k] = 0.0;
-        if (R.pin[k] >= 0)
-            bwd_gather<HARD, GRAD>(C, R.pin[k], R.fl[k], R.o1t[k], R.o1a[k], R.e1[k], c, t, r0[k],
-                                   rto[k], ado[k], nd[k], at[k], adj0[k], lse[k], epl[k], dout[k]);
-        if (R.arc[k] >= 0) wgt[k] = LDG(C.weights + (size_t)R.arc[k] * 2 + j);
+        if (STATIC) {
+            if (R.pin[k] >= 0) {
+                const int pin = R.pin[k], fl = R.fl[k];
+                ado[k] = R.ado[k]; nd[k] = R.nd[k]; at[k] = R.at[k];
+                lse[k] = R.lse[k]; epl[k] = R.epl[k]; r0[k] = R.r0[k];
+                if (HARD) {
+                    if (fl & TM_ROOT) r0[k] = LDG(C.required + (size_t)pin * 4 + c);
+                    if (R.o1a[k] >= 0) rto[k] = LDG(C.required + (size_t)R.o1t[k] * 4 + c);
+                }
+                if (GRAD && late) {
+                    if (fl & TM_ROOT) adj0[k] = LDG(C.adjoint + (size_t)pin * 2 + j);
+                    if (R.o1a[k] >= 0) dout[k] = LDG(C.d_arc + (size_t)R.o1a[k] * 2 + j);
+                }
+            }
+            wgt[k] = R.wgt[k];
+        } else {
+            if (R.pin[k] >= 0)
+                bwd_gather<HARD, GRAD>(C, R.pin[k], R.fl[k], R.o1t[k], R.o1a[k], R.e1[k], c, t, r0[k],
+                                       rto[k], ado[k], nd[k], at[k], adj0[k], lse[k], epl[k], dout[k]);
+            if (R.arc[k] >= 0) wgt[k] = LDG(C.weights + (size_t)R.arc[k] * 2 + j);
+        }
+    }
+    // (net, cond) item: the root's arrival (slack), init required and seed
+    double n_at = 0, n_rr = 0, n_seed = 0;
+    if (STATIC) {
+        n_at = R.n_at; n_rr = R.n_rr; n_seed = R.n_seed;
+    } else if (R.nroot >= 0) {
+        if (HARD) {
+            if (!(R.nflags & TQ_ROOT_MEMBER)) n_at = LDG(C.arrival + (size_t)R.nroot * 4 + c);
+            n_rr = root_init_required(t, C, R.nroot, R.nflags, R.ne1, c);
+        }
+        if (GRAD && late) n_seed = root_seed(t, C, R.nroot, R.nflags, R.ne1, j, g, kind);
     }
     __syncthreads();                                   // net records visible
+    BSTAMP(0);
     // ---- member phase
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
         if (R.pin[k] < 0) continue;
         const int mi = ii + k * TASK_Q, u = T.m0 + mi;
         double v = 0, de = 0;
-        bwd_member<HARD, GRAD>(t, C, u, R.pin[k], R.fl[k], c, g, kind, r0[k], rto[k], ado[k], nd[k],
-                               at[k], adj0[k], lse[k], epl[k], dout[k], v, de);
+        bwd_member<HARD, GRAD>(t, C, R.o0[k], R.o0[k] + R.no[k], R.pin[k], R.fl[k], c, g, kind, r0[k],
+                               rto[k], ado[k], nd[k], at[k], adj0[k], lse[k], epl[k], dout[k], v, de);
         const int qi = R.fl[k] >> 8;
         const size_t f = (size_t)(S.n.f0[qi] + (u - S.n.mptr[qi]));
         if (HARD) {
@@ -812,8 +997,8 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
         bwd_gather<HARD, GRAD>(C, pp, ff, t.tm_o1_to[u], t.tm_o1_arc[u], t.tm_e1[u], c, t, a_r0,
                                a_rto, a_ado, a_nd, a_at, a_adj0, a_lse, a_epl, a_dout);
         double v = 0, de = 0;
-        bwd_member<HARD, GRAD>(t, C, u, pp, ff, c, g, kind, a_r0, a_rto, a_ado, a_nd, a_at, a_adj0,
-                               a_lse, a_epl, a_dout, v, de);
+        bwd_member<HARD, GRAD>(t, C, t.tm_optr[u], t.tm_optr[u + 1], pp, ff, c, g, kind, a_r0, a_rto,
+                               a_ado, a_nd, a_at, a_adj0, a_lse, a_epl, a_dout, v, de);
         const size_t f = (size_t)(S.n.f0[0] + (u - S.n.mptr[0]));
         if (HARD) C.mem_buf[f * 4 + c] = v;
         if (GRAD && late) C.d_edge[f * 2 + j] = de;
@@ -826,6 +1011,7 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
             S.arc[ai] = R.arc[k];
         }
     __syncthreads();
+    BSTAMP(1);
     if (chunk) {
         // one chunk of a big star net: ordered partial folds, last chunk combines
         const int nch = t.bn_nch[T.slot];
@@ -878,7 +1064,7 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
         const int k0m = S.n.mptr[ii] - T.m0, k1m = S.n.mptr[ii + 1] - T.m0;
         if (HARD) {
             const bool mx = c < 2;
-            double rr = root_init_required(t, C, rt, fq, S.n.e1[ii], c);
+            double rr = n_rr;
             if (loop) {
                 const int s = S.n.f0[ii];
                 for (int k = 0; k < k1m - k0m; k++) {
@@ -890,13 +1076,11 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
                     if (later_wins(mx, rr, S.v[k * 4 + c])) rr = S.v[k * 4 + c];
             }
             C.required[(size_t)rt * 4 + c] = rr;
-            if (!(fq & TQ_ROOT_MEMBER)) {
-                const double a = LDG(C.arrival + (size_t)rt * 4 + c);
-                C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(a, rr) : __dsub_rn(rr, a);
-            }
+            if (!(fq & TQ_ROOT_MEMBER))
+                C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(n_at, rr) : __dsub_rn(rr, n_at);
         }
         if (GRAD && late) {
-            double ar = root_seed(t, C, rt, fq, S.n.e1[ii], j, g, kind);
+            double ar = n_seed;
             if ((fq & TQ_TREE) || loop) {
                 // parents gather children, deepest member first (diff.py:222-233)
                 const int s = S.n.f0[ii];
@@ -928,6 +1112,67 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
         }
     }
     __syncthreads();                         // smem reusable by the next task
+}
+
+// ---- streaming RC (reduce width 8) --------------------------------------
+// The RC stage has no level dependencies, so it runs as one HBM-streaming
+// launch instead of per-task blocks: blocks [0, nbm) take RC_ITEMS
+// (member, cond) items per thread in flat member order (mem_res / mem_cap
+// read once, fully coalesced); blocks [nbm, ..) take one (net, cond) item:
+// the root load of a star net (root_cap + root_load8 over its contiguous
+// member caps), or the whole Elmore recursion of a tree net.
+constexpr int RC_TPB = 256, RC_ITEMS = 4;
+
+__global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
+{
+    pdl_trigger();
+    const Corner& C = cs.c[blockIdx.y];
+    if ((int)blockIdx.x < nbm) {
+        const size_t base = (size_t)blockIdx.x * RC_TPB * RC_ITEMS + threadIdx.x;
+        const size_t n4 = (size_t)t.M * 4;
+        int code[RC_ITEMS];
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            const size_t i = base + (size_t)k * RC_TPB;
+            code[k] = i < n4 ? LDG(t.rc_code + (i >> 2)) : -1;
+        }
+        pdl_wait();
+        double b[RC_ITEMS], r[RC_ITEMS];
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            const size_t i = base + (size_t)k * RC_TPB;
+            b[k] = r[k] = 0.0;
+            if (code[k] >= 0) { b[k] = LDG(C.mem_cap + i); r[k] = LDG(C.mem_res + i); }
+        }
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            if (code[k] < 0) continue;
+            const int c = (int)((base + (size_t)k * RC_TPB) & 3);
+            const double d = __dadd_rn(0.0, __dmul_rn(r[k], b[k]));
+            const double rad = __dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, r[k]), b[k]), d), __dmul_rn(d, d));
+            const size_t pin = (size_t)(code[k] >> 1);
+            if (!(code[k] & 1)) C.load[pin * 4 + c] = b[k];
+            C.net_delay[pin * 4 + c] = d;
+            C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+        }
+        return;
+    }
+    const int i = ((int)blockIdx.x - nbm) * RC_TPB + threadIdx.x;
+    const int n = i >> 2, c = i & 3;
+    if (n >= t.N) return;
+    const int s = LDG(t.net_ptr + n), m = LDG(t.net_ptr + n + 1) - s, root = LDG(t.net_root + n);
+    const bool tree = LDG(t.net_tree + n), rm = LDG(t.member_of_pin + root) >= 0;
+    pdl_wait();
+    if (tree) {
+        rc_seq(t, C, n, root, s, m, c, 8, rm);
+        return;
+    }
+    const double l = root_load8(C.mem_cap + (size_t)s * 4 + c, 4, m);
+    C.load[(size_t)root * 4 + c] = __dadd_rn(LDG(C.root_cap + (size_t)n * 4 + c), l);
+    if (!rm) {
+        C.net_delay[(size_t)root * 4 + c] = 0.0;
+        C.impulse[(size_t)root * 4 + c] = 0.0;
+    }
 }
 
 // ---- per-level kernels (one task per block; PDL prologue = records) --------
@@ -1214,40 +1459,74 @@ __global__ void k_perturb(int M, int N, Corner D, Corner S, unsigned long long s
 // first task of the next level (static topology), so after the barrier only
 // the gathers of the just-finished level remain on the critical path.
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p)
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p)
 {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
-// sense-free generation barrier over the `n` blocks of one corner; all of
-// them are co-resident (cooperative launch).  The gpu-scope fences order
-// each block's writes before the barrier and (CCTL.IVALL) drop stale L1 lines.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned n)
+// Split grid barrier over the `n` blocks of one corner (all co-resident:
+// cooperative launch).  grid_arrive() publishes this block's writes and
+// returns the counter value that completes the barrier; the caller may do
+// independent work (prefetch the next level's records) before grid_wait().
+// The counter only grows, so no reset / generation word is needed.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* ctr, unsigned n,
+                                                          unsigned long long* s_target)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned gen = ld_acquire(bar + 1);
         __threadfence();
-        if (atomicAdd(bar, 1u) == n - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (ld_acquire(bar + 1) == gen) { }
-        }
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        *s_target = (old / n + 1) * n;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ void grid_wait(unsigned long long* ctr, unsigned long long* s_target)
+{
+    if (threadIdx.x == 0) {
+        const unsigned long long target = *s_target;
+        while (ld_acquire64(ctr) < target) { }
         __threadfence();
     }
     __syncthreads();
 }
 
+__device__ __forceinline__ void grid_sync(unsigned long long* ctr, unsigned n, unsigned long long* s_target)
+{
+    grid_arrive(ctr, n, s_target);
+    grid_wait(ctr, s_target);
+}
+
 union PassSmem {
-    RcSmem r;
     FwdSmem f;
     BwdSmem b;
     SumSmem s;
 };
+
+#ifdef WS_PROBE
+#define PSTAMP(level, slot)                                                                   \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && t.probe) {                                                    \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[((size_t)(level) * 2048 + blockIdx.x) * 4 + (slot)] = _v;                 \
+        }                                                                                     \
+    } while (0)
+// whole-kernel phases: 0 start | 1 RC done | 2 forward done | 3 backward done
+#define KSTAMP(slot)                                                                          \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && t.probe) {                                                    \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[(size_t)4 * t.L * 2048 * 4 + (size_t)blockIdx.x * 4 + (slot)] = _v;       \
+        }                                                                                     \
+    } while (0)
+#else
+#define PSTAMP(level, slot) do { } while (0)
+#define KSTAMP(slot) do { } while (0)
+#endif
 
 template <bool LSE, bool GRAD>
 __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners cs, SumArgs P,
@@ -1256,42 +1535,42 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PassSmem S;
     const Corner& C = cs.c[blockIdx.y];
-    unsigned* bar = C.sync_ctr + 1;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(C.sync_ctr + 2);
+    __shared__ unsigned long long s_target;
     const int cta = blockIdx.x, ncta = gridDim.x;
+    KSTAMP(0);
     const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
-    // ---- pins in no net, RC of every net
-    for (int i = cta * PASS_TPB + threadIdx.x; i < t.n_free; i += ncta * PASS_TPB)
-        free_pin(t, C, i, LSE);
-    for (int k = cta; k < t.n_tasks; k += ncta) {
-        const Task T = load_task(t, k);
-        RcRec R;
-        rc_records(t, T, S.r, R);
-        rc_body(t, C, T, S.r, R, w);
-    }
+    // pins in no net and the RC of every net ran as ordinary (fully
+    // parallel) kernels before this launch: RC is static for the pass
     // ---- forward levels
     {
         int k = t.lvt_ptr[0] + cta;
         bool have = t.L > 0 && k < t.lvt_ptr[1];
         Task T{};
         FwdRec R;
-        if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
-        grid_sync(bar, ncta);
+        KSTAMP(1);
+        if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
         for (int li = 0; li < t.L; li++) {
             const int kend = t.lvt_ptr[li + 1];
+            PSTAMP(li, 0);
             while (have) {
-                fwd_body<true, LSE>(t, L, C, T, S.f, R, g);
+                fwd_body<true, LSE, true>(t, L, C, T, S.f, R, g, li);
                 k += ncta;
                 have = k < kend;
-                if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
+                if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
             }
-            if (li + 1 < t.L) {
+            PSTAMP(li, 1);
+            grid_arrive(bar, ncta, &s_target);
+            if (li + 1 < t.L) {          // overlaps the barrier: static data only
                 k = t.lvt_ptr[li + 1] + cta;
                 have = k < t.lvt_ptr[li + 2];
-                if (have) { T = load_task(t, k); fwd_records<true>(t, T, S.f, R); }
+                if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
             }
-            grid_sync(bar, ncta);
+            PSTAMP(li, 2);
+            grid_wait(bar, &s_target);
         }
     }
+    KSTAMP(2);
     // ---- backward levels
     {
         const int variant = GRAD ? 3 : 1;
@@ -1300,23 +1579,28 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners
         bool have = li >= 0 && k < t.lvt_ptr[li + 1];
         Task T{};
         BwdRec R;
-        if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+        if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
         for (; li >= 0; li--) {
             const int kend = t.lvt_ptr[li + 1];
+            PSTAMP(t.L + li, 0);
             while (have) {
-                bwd_body<true, GRAD>(t, C, T, S.b, R, g, kind, variant);
+                bwd_body<true, GRAD, true>(t, C, T, S.b, R, g, kind, variant, t.L + li);
                 k += ncta;
                 have = k < kend;
-                if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+                if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
             }
-            if (li > 0) {
+            PSTAMP(t.L + li, 1);
+            grid_arrive(bar, ncta, &s_target);
+            if (li > 0) {                // overlaps the barrier: static data only
                 k = t.lvt_ptr[li - 1] + cta;
                 have = k < t.lvt_ptr[li];
-                if (have) { T = load_task(t, k); bwd_records<GRAD>(t, T, S.b, R); }
+                if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
             }
-            grid_sync(bar, ncta);
+            PSTAMP(t.L + li, 2);
+            grid_wait(bar, &s_target);
         }
     }
+    KSTAMP(3);
     // ---- pins finished after the level loop, then TNS / WNS / loss
     if (GRAD)
         for (int i = cta * PASS_TPB + threadIdx.x; i < 2 * t.n_fin; i += ncta * PASS_TPB)
@@ -1434,7 +1718,7 @@ struct Launcher {
         ls = {t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, t.NL,
               ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len, t.lut_info};
         lut_bytes = lut_smem_bytes(t.NL, ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len);
-        use_smem = lut_bytes <= 96 * 1024;
+        use_smem = lut_bytes <= 96 * 1024 && !ctx.lut_global;
         if (!use_smem) lut_bytes = 0;
     }
     dim3 grid1(int n, int tpb) const { return dim3((unsigned)std::max(1, (n + tpb - 1) / tpb), nc); }
@@ -1449,7 +1733,13 @@ struct Launcher {
     void rc(cudaStream_t s, int w)
     {
         if (!ctx.t.n_tasks) return;
-        launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
+        if (w == 8) {
+            const int nbm = (int)(((size_t)ctx.t.M * 4 + RC_TPB * RC_ITEMS - 1) / (RC_TPB * RC_ITEMS));
+            const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
+            launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm);
+        } else {
+            launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
+        }
         count++;
     }
     // WS_PROBE builds: launch i stamps into probe + i * PROBE_STRIDE
@@ -1560,6 +1850,8 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
     const bool two = (flags & WS_RUN_TWO_STREAM) && hard && (lse || grad) && !fused;
 
     if ((flags & WS_RUN_PERSISTENT) && hard && ((lse && grad) || (!lse && !grad))) {
+        la.free_pins(s, lse);
+        la.rc(s, w);
         if (lse) la.persistent<true, true>(s, w, g, kind);
         else la.persistent<false, false>(s, w, g, kind);
     } else if (fused) {
