@@ -121,10 +121,13 @@ def reference_flat(raw):
     flatten (pinned bit-exact to the reference's flatten by
     tests/test_oracle_golden.py) — the reference's own flatten() would need
     ~100 s of Python object construction at C3."""
-    ref = os.path.join(REPO, "oracle", "_ref")
     from oracle import oracle as O
     of = O.flatten_raw(raw)
-    if os.path.isdir(os.path.join(ref, "stasim")):
+    # the pip-installed unmodified reference (baseline/_ref, see DESIGN.md §7),
+    # else the same sources built by oracle/build_ref.sh
+    ref = next((d for d in (os.path.join(REPO, "baseline", "_ref"), os.path.join(REPO, "oracle", "_ref"))
+                if os.path.isdir(os.path.join(d, "stasim"))), None)
+    if ref is not None:
         sys.path.insert(0, ref)
         import stasim  # the unmodified reference
         from stasim.flatten import FlatDesign, LevelSchedule

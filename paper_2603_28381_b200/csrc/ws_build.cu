@@ -383,6 +383,15 @@ int reduce_max(Scratch& sc, Arena& ar, const int* a, int n, cudaStream_t s)
     return h;
 }
 
+// delay LUT ids of each task net's first in-arc (the root-load locate axis)
+__global__ void k_tq_lut1(int N, const int* tq_aptr, const ushort4* ta_lut, ushort4* out)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= N) return;
+    out[q] = tq_aptr[q + 1] > tq_aptr[q] ? ta_lut[2 * (size_t)tq_aptr[q]]
+                                         : make_ushort4(0xffff, 0xffff, 0xffff, 0xffff);
+}
+
 // streaming-RC member code: -1 for members of tree nets (handled per net),
 // else pin << 1 | (pin roots a net: its load comes from that net)
 __global__ void k_rc_code(int M, const int* mem_pin, const int* mem_net, const int* net_tree,
@@ -455,6 +464,11 @@ void build_tasks(Context& ctx)
                                            t.root_net_of_pin, t.pin_ep_ptr, t.pin_ep_idx,
                                            t.mem_out_ptr, t.mem_out_arc, t.arc_to, t.tm_pin,
                                            t.tm_flags, t.tm_o1_to, t.tm_o1_arc, t.tm_e1, ocnt);
+        WS_CHECK_LAUNCH();
+    }
+    t.tq_lut1 = ar.alloc<ushort4>(N);
+    if (N) {
+        k_tq_lut1<<<blocks_for(N), TPB, 0, s>>>(N, t.tq_aptr, t.ta_lut, t.tq_lut1);
         WS_CHECK_LAUNCH();
     }
     scan(ocnt, t.tm_optr, M);
@@ -831,6 +845,8 @@ void build_topology(Context& ctx, const ws_design_desc* d)
         }
         ctx.lv_maxm_host.assign(t.L, 0);
         ctx.lv_tree_host.assign(t.L, 0);
+        ctx.any_tree = false;
+        for (int n = 0; n < N; n++) ctx.any_tree |= tr[n] != 0;
         for (int li = 0; li < t.L; li++)
             for (int q = ctx.lv_ptr_host[li]; q < ctx.lv_ptr_host[li + 1]; q++) {
                 ctx.lv_maxm_host[li] = std::max(ctx.lv_maxm_host[li], nm[lvn[q]]);

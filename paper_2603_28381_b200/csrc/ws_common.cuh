@@ -72,6 +72,7 @@ struct Topo {
     int *ta_root;      // [A'] root pin of the arc's net
     int *ta_q;         // [A'] index of the arc's net within its task
     ushort4 *ta_lut;   // [2*A'] delay LUT ids (ER EF LR LF), then slew LUT ids
+    ushort4 *tq_lut1;  // [N] delay LUT ids of q's first in-arc (0xffff: no in-arc)
     int *tm_pin;       // [M] member pin
     int *tm_flags;     // [M] TM_* bits | (net index within its task) << 8
     int *tm_optr;      // [M+1] out-arcs of member slot u: to_*[tm_optr[u] .. )

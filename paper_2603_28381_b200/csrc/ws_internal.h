@@ -94,7 +94,8 @@ struct Context {
     int lut_t_len = 0, lut_s_len = 0, lut_l_len = 0;
     std::vector<int> lv_ptr_host;     // L+1
     std::vector<int> lv_maxm_host;    // per level: max member count
-    std::vector<int> lv_tree_host;    // per level: any tree net
+    std::vector<int> lv_tree_host;     // per level: any tree net
+    bool any_tree = false;             // any net with a non-root parent (k_rc_tree needed)
     std::vector<int> lvt_ptr_host;    // per level: first task (L+1)
     cudaStream_t s_main = nullptr, s_grad = nullptr;
     std::vector<cudaEvent_t> events;

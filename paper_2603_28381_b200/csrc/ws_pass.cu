@@ -1137,12 +1137,13 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
             code[k] = i < n4 ? LDG(t.rc_code + (i >> 2)) : -1;
         }
         pdl_wait();
+        // values loaded independently of the codes: one round trip
         double b[RC_ITEMS], r[RC_ITEMS];
 #pragma unroll
         for (int k = 0; k < RC_ITEMS; k++) {
             const size_t i = base + (size_t)k * RC_TPB;
             b[k] = r[k] = 0.0;
-            if (code[k] >= 0) { b[k] = LDG(C.mem_cap + i); r[k] = LDG(C.mem_res + i); }
+            if (i < n4) { b[k] = __ldcs(C.mem_cap + i); r[k] = __ldcs(C.mem_res + i); }
         }
 #pragma unroll
         for (int k = 0; k < RC_ITEMS; k++) {
@@ -1160,19 +1161,36 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
     const int i = ((int)blockIdx.x - nbm) * RC_TPB + threadIdx.x;
     const int n = i >> 2, c = i & 3;
     if (n >= t.N) return;
+    if (LDG(t.net_tree + n)) return;             // k_rc_tree
     const int s = LDG(t.net_ptr + n), m = LDG(t.net_ptr + n + 1) - s, root = LDG(t.net_root + n);
-    const bool tree = LDG(t.net_tree + n), rm = LDG(t.member_of_pin + root) >= 0;
+    const bool rm = LDG(t.member_of_pin + root) >= 0;
     pdl_wait();
-    if (tree) {
-        rc_seq(t, C, n, root, s, m, c, 8, rm);
-        return;
-    }
     const double l = root_load8(C.mem_cap + (size_t)s * 4 + c, 4, m);
     C.load[(size_t)root * 4 + c] = __dadd_rn(LDG(C.root_cap + (size_t)n * 4 + c), l);
     if (!rm) {
         C.net_delay[(size_t)root * 4 + c] = 0.0;
         C.impulse[(size_t)root * 4 + c] = 0.0;
     }
+}
+
+// tree nets (any member with a non-root parent): the whole Elmore recursion
+// per (net, cond), sequential like the reference
+__global__ void __launch_bounds__(RC_TPB) k_rc_tree(Topo t, Corners cs)
+{
+    pdl_trigger();
+    const Corner& C = cs.c[blockIdx.y];
+    const int i = blockIdx.x * RC_TPB + threadIdx.x;
+    const int n = i >> 2, c = i & 3;
+    bool tree = false;
+    int s = 0, m = 0, root = 0;
+    if (n < t.N && LDG(t.net_tree + n)) {
+        tree = true;
+        s = LDG(t.net_ptr + n);
+        m = LDG(t.net_ptr + n + 1) - s;
+        root = LDG(t.net_root + n);
+    }
+    pdl_wait();
+    if (tree) rc_seq(t, C, n, root, s, m, c, 8, LDG(t.member_of_pin + root) >= 0);
 }
 
 // ---- per-level kernels (one task per block; PDL prologue = records) --------
@@ -1737,6 +1755,10 @@ struct Launcher {
             const int nbm = (int)(((size_t)ctx.t.M * 4 + RC_TPB * RC_ITEMS - 1) / (RC_TPB * RC_ITEMS));
             const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
             launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm);
+            if (ctx.any_tree) {
+                count++;
+                launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);
+            }
         } else {
             launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
         }
