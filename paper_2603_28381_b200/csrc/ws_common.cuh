@@ -184,6 +184,16 @@ struct Loc {
     double f;
 };
 
+static __device__ __noinline__ int upper_bound_long(const double* ax, int n, double q)
+{
+    int hi = n, lo = 0;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ax[mid] <= q) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
 {
     Loc r;
@@ -196,12 +206,7 @@ __device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
 #pragma unroll
             for (int k = 0; k < 8; k++) lo += (k < n && ax[k] <= q) ? 1 : 0;
         } else {
-            int hi = n;
-            lo = 0;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (ax[mid] <= q) lo = mid + 1; else hi = mid;
-            }
+            lo = upper_bound_long(ax, n, q);
         }
         int i = lo - 1;
         if (i < 0) i = 0; else if (i > n - 2) i = n - 2;

@@ -390,28 +390,30 @@ __device__ void rc_body(const Topo& t, const Corner& C, const Task& T, RcSmem& S
 }
 
 // ---- forward level (forward_level, _kernels.pyx:159-210) + LSE (diff.py:123-146)
+//
+// Net-centric: the thread of (net, cond) item (qi, c) evaluates all in-arcs
+// of its net itself (generated netlists have <= 3 in-arcs per net; up to
+// FWD_NA are held in registers, more take a loop over global records), so
+// the arc delays, the ordered max/min merge, the winner's output slew and
+// the whole LSE (max, exp, reduceat sum, log, softmax weights) need no
+// shared-memory exchange and no barrier.  One barrier then publishes the
+// root results to the member phase.
+
+constexpr int FWD_NA = 3;
 
 struct FwdSmem {
     NetSmem n;
-    double cand[TASK_A * 4];    // arrival candidate of (arc, cond)
-    double sw[TASK_A * 4];      // output slew if the arc wins (speculative, parallel)
-    double x[TASK_A * 2];       // LSE operand of (arc, late col)
-    double z[TASK_A * 2];       // exp((x - c) / gamma)
-    double cm[TASK_Q * 2];      // LSE max per (net, late col)
-    double ss[TASK_Q * 2];      // LSE denominator
     double at[TASK_Q * 4], sl[TASK_Q * 4], lr[TASK_Q * 2];   // root results
-    double lf[TASK_Q * 4];      // load-axis locate of the root load (per net, cond) ...
-    int li[TASK_Q * 4];         // ... index, and the canonical axis it was taken on
-    int lax[TASK_Q * 4];
 };
 
 struct FwdRec {
-    int from[ITEMS], root[ITEMS], arc[ITEMS], aq[ITEMS];
-    unsigned short dl[ITEMS], sl[ITEMS];
+    int na, a0;                       // the net item's in-arcs: ta_*[a0 .. a0 + na)
+    int from[FWD_NA], arc[FWD_NA];
+    unsigned short dl[FWD_NA], sl[FWD_NA];
     int mpin[ITEMS], mfl[ITEMS];
-    int nroot, nflags, nlut;    // this lane's (net, cond) item: root, flags, first arc's delay LUT
+    int nroot, nflags;                // this lane's (net, cond) item
     // pass-static gathers (RC outputs), prefetched by the persistent kernel
-    double ld[ITEMS], mnd[ITEMS], mim[ITEMS];
+    double ld, mnd[ITEMS], mim[ITEMS];
 };
 
 // numpy's np.add.reduceat segment: z_0 + pairwise_sum(z_1 .. z_{n-1})
@@ -435,76 +437,39 @@ __device__ __forceinline__ double reduceat_sum(const double* z, int stride, int 
 }
 
 template <bool HARD>
-__device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R);
-
-// the (net, cond) item's root load located on its first arc's load axis
-__device__ __forceinline__ void net_load_locate(const Topo& t, const Corner& C, const FwdRec& R,
-                                                FwdSmem& S, int ii, int c)
-{
-    if (R.nroot < 0 || (R.nflags & TQ_KIND) != ROOT_ARC) return;
-    if (R.nlut >= 0) {
-        const int4 inf = t.lut_info[R.nlut];
-        const Loc lc = lut_locate(t.lut_l_flat + inf.z, inf.w, LDG(C.load + (size_t)R.nroot * 4 + c));
-        S.lf[ii * 4 + c] = lc.f;
-        S.li[ii * 4 + c] = lc.i0 | (lc.i1 << 16);
-        S.lax[ii * 4 + c] = inf.z | (inf.w << 24);
-    } else {
-        S.lax[ii * 4 + c] = -1;
-    }
-}
-
-// persistent kernel: records plus every gather that is static for the whole
-// forward sweep (RC outputs) and the root-load locate
-template <bool HARD>
-__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, const Task& T,
-                                                   FwdSmem& S, FwdRec& R)
-{
-    fwd_records<HARD>(t, T, S, R);
-    const int c = threadIdx.x & 3;
-#pragma unroll
-    for (int k = 0; k < ITEMS; k++) {
-        if (HARD && R.arc[k] >= 0) R.ld[k] = LDG(C.load + (size_t)R.root[k] * 4 + c);
-        if (R.mpin[k] >= 0) {
-            R.mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
-            if (HARD) R.mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
-        }
-    }
-    if (HARD) net_load_locate(t, C, R, S, threadIdx.x >> 2, c);
-}
-
-template <bool HARD>
 __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R)
 {
     load_nets(t, T, S.n);
-    const int c = threadIdx.x & 3;
+    const int c = threadIdx.x & 3, qi = threadIdx.x >> 2;
     const bool wide = T.flags & TK_WIDE;
     R.nroot = -1;
-    {
-        const int qi = threadIdx.x >> 2;
-        if (qi < T.nq) {
-            const int q = T.q0 + qi;
-            R.nroot = t.tq_root[q];
-            R.nflags = t.tq_flags[q];
-            R.nlut = -1;
-            if (HARD && (R.nflags & TQ_KIND) == ROOT_ARC && !wide)
-                R.nlut = lut_c(t.ta_lut[2 * (size_t)t.tq_aptr[q]], c);
+    R.na = 0;
+    if (qi < T.nq) {
+        const int q = T.q0 + qi;
+        R.nroot = t.tq_root[q];
+        R.nflags = t.tq_flags[q];
+        if ((R.nflags & TQ_KIND) == ROOT_ARC && !wide) {
+            R.a0 = t.tq_aptr[q];
+            R.na = t.tq_aptr[q + 1] - R.a0;
+            if (R.na > 0 && R.na <= FWD_NA) {
+                // slots past the last arc repeat arc 0: the net phase then
+                // runs FWD_NA independent chains without branches
+#pragma unroll
+                for (int k = 0; k < FWD_NA; k++) {
+                    const int qa = R.a0 + (k < R.na ? k : 0);
+                    R.from[k] = t.ta_from[qa];
+                    R.arc[k] = t.ta_arc[qa];
+                    if (HARD) {
+                        R.dl[k] = lut_c(t.ta_lut[2 * (size_t)qa], c);
+                        R.sl[k] = lut_c(t.ta_lut[2 * (size_t)qa + 1], c);
+                    }
+                }
+            }
         }
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
-        const int ii = (threadIdx.x >> 2) + k * TASK_Q;
-        R.arc[k] = -1;
-        if (ii < T.na && !wide) {
-            const int q = T.a0 + ii;
-            R.from[k] = t.ta_from[q];
-            R.root[k] = t.ta_root[q];
-            R.arc[k] = t.ta_arc[q];
-            R.aq[k] = t.ta_q[q];
-            if (HARD) {
-                R.dl[k] = lut_c(t.ta_lut[2 * (size_t)q], c);
-                R.sl[k] = lut_c(t.ta_lut[2 * (size_t)q + 1], c);
-            }
-        }
+        const int ii = qi + k * TASK_Q;
         R.mpin[k] = -1;
         if (ii < T.nm) {
             R.mpin[k] = t.tm_pin[T.m0 + ii];
@@ -513,29 +478,109 @@ __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSme
     }
 }
 
+// persistent kernel: records plus every gather that is static for the whole
+// forward sweep (RC outputs)
+template <bool HARD>
+__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, const Task& T,
+                                                   FwdSmem& S, FwdRec& R)
+{
+    fwd_records<HARD>(t, T, S, R);
+    const int c = threadIdx.x & 3;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++)
+        if (R.mpin[k] >= 0) {
+            R.mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
+            if (HARD) R.mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
+        }
+    R.ld = (HARD && R.na > 0) ? LDG(C.load + (size_t)R.nroot * 4 + c) : 0.0;
+}
+
+// arc-driven root with more than FWD_NA (but <= TASK_A) in-arcs: the same
+// arithmetic in the same order, records read in a loop
+template <bool HARD, bool LSE>
+__device__ void fwd_net_loop(const Topo& t, const LutView& L, const Corner& C, int a0, int a1, int rt,
+                             double ld, int c, double g, bool first, double& at, double& sl, double& lr)
+{
+    const bool late = c >= 2;
+    if (HARD) {
+        double best = late ? -INF : INF;
+        int wq = a0;
+        for (int q = a0; q < a1; q++) {
+            const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], c),
+                                        LDG(C.slew + (size_t)t.ta_from[q] * 4 + c), ld);
+            C.arc_delay[(size_t)t.ta_arc[q] * 4 + c] = d;
+            const double v = __dadd_rn(LDG(C.arrival + (size_t)t.ta_from[q] * 4 + c), d);
+            if (later_wins(late, best, v)) { best = v; wq = q; }
+        }
+        at = best;
+        sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c), LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), ld);
+    }
+    if (LSE && late) lr = lse_root_global(t, C, a0, a1, c, g, first);
+}
+
+// the root of a TK_WIDE task (> TASK_A in-arcs): arc delays are in global
+template <bool HARD, bool LSE>
+__device__ void fwd_net_wide(const Topo& t, const LutView& L, const Corner& C, int qa0, int qa1,
+                                          int rt, int c, double g, bool first, double& at, double& sl,
+                                          double& lr)
+{
+    const bool late = c >= 2;
+    if (HARD) {
+        double best = late ? -INF : INF;
+        int wq = qa0;
+        for (int q = qa0; q < qa1; q++) {
+            const double v = __dadd_rn(LDG(C.arrival + (size_t)t.ta_from[q] * 4 + c),
+                                       LDG(C.arc_delay + (size_t)t.ta_arc[q] * 4 + c));
+            if (later_wins(late, best, v)) { best = v; wq = q; }
+        }
+        at = best;
+        sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c),
+                        LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), LDG(C.load + (size_t)rt * 4 + c));
+    }
+    if (LSE && late) lr = lse_root_global(t, C, qa0, qa1, c, g, first);
+}
+
+// arc delays of a TK_WIDE task, all block threads
+__device__ void fwd_wide_delays(const Topo& t, const LutView& L, const Corner& C, const Task& T,
+                                             int rt)
+{
+    for (int i = threadIdx.x; i < T.na * 4; i += blockDim.x) {
+        const int q = T.a0 + (i >> 2), cc = i & 3;
+        const int fp = t.ta_from[q];
+        const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], cc),
+                                    LDG(C.slew + (size_t)fp * 4 + cc), LDG(C.load + (size_t)rt * 4 + cc));
+        C.arc_delay[(size_t)t.ta_arc[q] * 4 + cc] = d;
+    }
+}
+
 template <bool HARD, bool LSE, bool STATIC = false>
 __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const Task& T,
                          FwdSmem& S, const FwdRec& R, double g, int plev = -1)
 {
-    const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
+    const int tid = threadIdx.x, c = tid & 3, qi = tid >> 2;
     const bool late = c >= 2;
     const int j = c - 2;
     const bool wide = T.flags & TK_WIDE;
     // ---- R3: every gather of the task at once
-    double slf[ITEMS], atf[ITEMS], ld[ITEMS], xl[ITEMS], dd[ITEMS], mnd[ITEMS], mim[ITEMS];
+    double slf[FWD_NA], atf[FWD_NA], xl[FWD_NA], dd[FWD_NA], mnd[ITEMS], mim[ITEMS];
+    double ld = 0;
 #pragma unroll
-    for (int k = 0; k < ITEMS; k++) {
-        slf[k] = atf[k] = ld[k] = xl[k] = dd[k] = mnd[k] = mim[k] = 0.0;
-        if (R.arc[k] >= 0) {
+    for (int k = 0; k < FWD_NA; k++) {
+        slf[k] = atf[k] = xl[k] = dd[k] = 0.0;
+        if (R.na > 0 && R.na <= FWD_NA) {
             if (HARD) {
                 slf[k] = LDG(C.slew + (size_t)R.from[k] * 4 + c);
                 atf[k] = LDG(C.arrival + (size_t)R.from[k] * 4 + c);
-                ld[k] = STATIC ? R.ld[k] : LDG(C.load + (size_t)R.root[k] * 4 + c);
             } else {
                 dd[k] = LDG(C.arc_delay + (size_t)R.arc[k] * 4 + c);
             }
             if (LSE && late) xl[k] = LDG(C.lse_at + (size_t)R.from[k] * 2 + j);
         }
+    }
+    if (HARD && R.na > 0) ld = STATIC ? R.ld : LDG(C.load + (size_t)R.nroot * 4 + c);
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        mnd[k] = mim[k] = 0.0;
         if (R.mpin[k] >= 0) {
             if (STATIC) {
                 mnd[k] = R.mnd[k];
@@ -546,20 +591,17 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
             }
         }
     }
-    // (net, cond) item: the root's load located once for all its arcs (on the
-    // first arc's delay-LUT load axis), and the seeds of non-arc-driven roots
+    // seeds of roots not driven by an in-arc
     double n_at = 0, n_sl = 0, n_lr = 0;
     if (R.nroot >= 0) {
         const int kind = R.nflags & TQ_KIND;
-        if (kind == ROOT_ARC) {
-            if (HARD && !STATIC) net_load_locate(t, C, R, S, ii, c);
-        } else if (kind == ROOT_FEED) {
+        if (kind == ROOT_FEED) {
             if (HARD) {
                 n_at = LDG(C.arrival + (size_t)R.nroot * 4 + c);
                 n_sl = LDG(C.slew + (size_t)R.nroot * 4 + c);
             }
             if (LSE && late) n_lr = LDG(C.lse_at + (size_t)R.nroot * 2 + j);
-        } else if (R.nflags & TQ_ROOT_PI) {
+        } else if (kind != ROOT_ARC && (R.nflags & TQ_ROOT_PI)) {
             const int pi = t.pin_pi[R.nroot];
             n_at = C.pi_arrival[(size_t)pi * 4 + c];
             n_sl = C.pi_slew[(size_t)pi * 4 + c];
@@ -567,111 +609,93 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
     }
     __syncthreads();                  // net records (and the LUT pool) visible
     BSTAMP(0);
-    // ---- arc phase: delay LUT, candidate, speculative output slew, LSE operand
-#pragma unroll
-    for (int k = 0; k < ITEMS; k++) {
-        if (R.arc[k] < 0) continue;
-        const int ai = ii + k * TASK_Q;
-        if (HARD) {
-            // delay and output-slew tables of this (arc, cond): one axis
-            // search serves both when their axes coincide
-            const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
-            const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
-            Loc lld;
-            const int nax = S.lax[R.aq[k] * 4 + c];
-            if (nax == (di.z | (di.w << 24))) {     // the net-level locate applies
-                const int pk = S.li[R.aq[k] * 4 + c];
-                lld.i0 = pk & 0xffff;
-                lld.i1 = pk >> 16;
-                lld.f = S.lf[R.aq[k] * 4 + c];
-            } else {
-                lld = lut_locate(L.l + di.z, di.w, ld[k]);
-            }
-            dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
-            const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
-            const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld[k]);
-            C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
-            S.cand[ai * 4 + c] = __dadd_rn(atf[k], dd[k]);
-            S.sw[ai * 4 + c] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
-        }
-        if (LSE && late) S.x[ai * 2 + j] = __dadd_rn(xl[k], dd[k]);
-    }
     if (HARD && wide) {
         // one net with > TASK_A in-arcs: arc delays in a loop, merge from global
-        const int rt = S.n.root[0];
-        for (int i = tid; i < T.na * 4; i += blockDim.x) {
-            const int q = T.a0 + (i >> 2), cc = i & 3;
-            const int fp = t.ta_from[q];
-            const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], cc),
-                                        LDG(C.slew + (size_t)fp * 4 + cc), LDG(C.load + (size_t)rt * 4 + cc));
-            C.arc_delay[(size_t)t.ta_arc[q] * 4 + cc] = d;
-        }
+        fwd_wide_delays(t, L, C, T, S.n.root[0]);
+        __syncthreads();
     }
-    __syncthreads();
     BSTAMP(1);
-    // ---- net phase 1: merge in arc order (first arc wins ties), LSE max
+    // ---- net phase: in-arcs of the own net, merge in arc order (first arc
+    // wins ties), winner's output slew, LSE
     const bool first = !(T.flags & TK_CHUNK) || T.m0 == S.n.mptr[0];
-    int kind = 0, a0 = 0, a1 = 0, rt = 0;
-    if (ii < T.nq) {
-        const int fl = S.n.flags[ii];
-        kind = fl & TQ_KIND;
-        rt = S.n.root[ii];
-        a0 = S.n.aptr[ii] - T.a0;
-        a1 = S.n.aptr[ii + 1] - T.a0;
-        double at = 0, sl = 0;
+    if (qi < T.nq) {
+        const int fl = S.n.flags[qi];
+        const int kind = fl & TQ_KIND;
+        const int rt = S.n.root[qi];
+        double at = 0, sl = 0, lr = 0;
         if (kind == ROOT_ARC) {
-            if (!wide) {
-                if (HARD) {
-                    double best = late ? -INF : INF;
-                    int wq = a0;
-                    for (int q = a0; q < a1; q++) {
-                        const double v = S.cand[q * 4 + c];
-                        if (later_wins(late, best, v)) { best = v; wq = q; }
-                    }
-                    at = best;
-                    sl = S.sw[wq * 4 + c];
-                }
-                if (LSE && late) {
-                    double cm = -INF;
-                    for (int q = a0; q < a1; q++) {
-                        const double x = S.x[q * 2 + j];
-                        if (q == a0 || x > cm) cm = x;   // np.maximum.reduceat
-                    }
-                    S.cm[ii * 2 + j] = cm;
-                }
+            if (wide) {
+                fwd_net_wide<HARD, LSE>(t, L, C, S.n.aptr[0], S.n.aptr[1], rt, c, g, first, at, sl, lr);
+            } else if (R.na > FWD_NA) {
+                fwd_net_loop<HARD, LSE>(t, L, C, R.a0, R.a0 + R.na, rt, ld, c, g, first, at, sl, lr);
             } else {
-                const int qa0 = S.n.aptr[0], qa1 = S.n.aptr[1];
                 if (HARD) {
+                    // every slot's delay and output slew (independent chains),
+                    // then the ordered merge; the root load is located once
+                    // on the first arc's load axis
+                    const int4 d0 = L.info[R.dl[0]];
+                    const Loc ll0 = lut_locate(L.l + d0.z, d0.w, ld);
+                    double sw[FWD_NA];
+#pragma unroll
+                    for (int k = 0; k < FWD_NA; k++) {
+                        const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
+                        const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
+                        const Loc lld = (di.z == d0.z && di.w == d0.w) ? ll0 : lut_locate(L.l + di.z, di.w, ld);
+                        dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
+                        const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
+                        const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld);
+                        sw[k] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
+                    }
                     double best = late ? -INF : INF;
-                    int wq = qa0;
-                    for (int q = qa0; q < qa1; q++) {
-                        const double v = __dadd_rn(LDG(C.arrival + (size_t)t.ta_from[q] * 4 + c),
-                                                   LDG(C.arc_delay + (size_t)t.ta_arc[q] * 4 + c));
-                        if (later_wins(late, best, v)) { best = v; wq = q; }
+                    sl = sw[0];
+#pragma unroll
+                    for (int k = 0; k < FWD_NA; k++) {
+                        if (k >= R.na) break;
+                        C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
+                        const double v = __dadd_rn(atf[k], dd[k]);
+                        if (later_wins(late, best, v)) { best = v; sl = sw[k]; }
                     }
                     at = best;
-                    sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c),
-                                    LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), LDG(C.load + (size_t)rt * 4 + c));
                 }
                 if (LSE && late) {
-                    const double lr = lse_root_global(t, C, qa0, qa1, c, g, first);
-                    S.lr[ii * 2 + j] = lr;
-                    if (first) C.lse_at[(size_t)rt * 2 + j] = lr;
+                    double x[FWD_NA], z[FWD_NA];
+                    double cm = -INF;
+#pragma unroll
+                    for (int k = 0; k < FWD_NA; k++) {
+                        x[k] = __dadd_rn(xl[k], dd[k]);
+                        if (k < R.na && (k == 0 || x[k] > cm)) cm = x[k];     // np.maximum.reduceat
+                    }
+#pragma unroll
+                    for (int k = 0; k < FWD_NA; k++) z[k] = exp(__ddiv_rn(__dsub_rn(x[k], cm), g));
+                    double rest = 0.0;
+#pragma unroll
+                    for (int k = 1; k < FWD_NA; k++)
+                        if (k < R.na) rest = __dadd_rn(rest, z[k]);   // reduceat: z0 + sequential (n < 9)
+                    const double s = __dadd_rn(z[0], rest);
+                    lr = __dadd_rn(cm, __dmul_rn(g, log(s)));
+                    if (first)
+#pragma unroll
+                        for (int k = 0; k < FWD_NA; k++)
+                            if (k < R.na) C.weights[(size_t)R.arc[k] * 2 + j] = __ddiv_rn(z[k], s);
                 }
             }
-            if (first && HARD) {
-                C.arrival[(size_t)rt * 4 + c] = at;
-                C.slew[(size_t)rt * 4 + c] = sl;
+            if (first) {
+                if (HARD) {
+                    C.arrival[(size_t)rt * 4 + c] = at;
+                    C.slew[(size_t)rt * 4 + c] = sl;
+                }
+                if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = lr;
             }
         } else if (kind == ROOT_FEED) {
             // driven by its parent net's member update (a lower level)
             at = n_at;
             sl = n_sl;
-            if (LSE && late) S.lr[ii * 2 + j] = n_lr;
+            lr = n_lr;
         } else {
             // primary-input root (or undriven): the seeded values
             at = n_at;
             sl = n_sl;
+            lr = at;
             if (first) {
                 if (HARD) {
                     C.arrival[(size_t)rt * 4 + c] = at;
@@ -679,64 +703,36 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
                 }
                 if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = at;
             }
-            if (LSE && late) S.lr[ii * 2 + j] = at;
         }
-        if (HARD) { S.at[ii * 4 + c] = at; S.sl[ii * 4 + c] = sl; }
-    }
-    if (LSE && !wide) {
-        __syncthreads();
-        // ---- arc phase 2: z = exp((x - c) / gamma), all arcs in parallel
-        if (late)
-#pragma unroll
-            for (int k = 0; k < ITEMS; k++) {
-                if (R.arc[k] < 0) continue;
-                const int ai = ii + k * TASK_Q;
-                S.z[ai * 2 + j] = exp(__ddiv_rn(__dsub_rn(S.x[ai * 2 + j], S.cm[R.aq[k] * 2 + j]), g));
-            }
-        __syncthreads();
-        // ---- net phase 2: denominator and smooth max
-        if (ii < T.nq && late && kind == ROOT_ARC) {
-            const double s = reduceat_sum(S.z + a0 * 2 + j, 2, a1 - a0);
-            const double lr = __dadd_rn(S.cm[ii * 2 + j], __dmul_rn(g, log(s)));
-            S.ss[ii * 2 + j] = s;
-            S.lr[ii * 2 + j] = lr;
-            if (first) C.lse_at[(size_t)rt * 2 + j] = lr;
-        }
+        if (HARD) { S.at[qi * 4 + c] = at; S.sl[qi * 4 + c] = sl; }
+        if (LSE && late) S.lr[qi * 2 + j] = lr;
     }
     __syncthreads();
     BSTAMP(2);
-    // ---- arc phase 3: softmax weights (alongside the member phase)
-    if (LSE && !wide && first && late)
-#pragma unroll
-        for (int k = 0; k < ITEMS; k++) {
-            if (R.arc[k] < 0) continue;
-            const int ai = ii + k * TASK_Q;
-            C.weights[(size_t)R.arc[k] * 2 + j] = __ddiv_rn(S.z[ai * 2 + j], S.ss[R.aq[k] * 2 + j]);
-        }
     // ---- member phase: one (member, cond) per item
 #pragma unroll
     for (int k = 0; k < ITEMS; k++) {
         if (R.mpin[k] < 0) continue;
         const size_t pin = (size_t)R.mpin[k];
-        const int qi = R.mfl[k] >> 8;
+        const int mq = R.mfl[k] >> 8;
         if (HARD) {
-            const double sr = S.sl[qi * 4 + c];
-            C.arrival[pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], mnd[k]);
+            const double sr = S.sl[mq * 4 + c];
+            C.arrival[pin * 4 + c] = __dadd_rn(S.at[mq * 4 + c], mnd[k]);
             C.slew[pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(mim[k], mim[k])));
         }
-        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[qi * 2 + j], mnd[k]);
+        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[mq * 2 + j], mnd[k]);
     }
     for (int i = tid + ITEMS * PASS_TPB; i < T.nm * 4; i += blockDim.x) {   // TK_LOOP tasks
         const int u = T.m0 + (i >> 2);
         const size_t pin = (size_t)t.tm_pin[u];
-        const int qi = t.tm_flags[u] >> 8;
+        const int mq = t.tm_flags[u] >> 8;
         const double nd = LDG(C.net_delay + pin * 4 + c);
         if (HARD) {
-            const double sr = S.sl[qi * 4 + c], im = LDG(C.impulse + pin * 4 + c);
-            C.arrival[pin * 4 + c] = __dadd_rn(S.at[qi * 4 + c], nd);
+            const double sr = S.sl[mq * 4 + c], im = LDG(C.impulse + pin * 4 + c);
+            C.arrival[pin * 4 + c] = __dadd_rn(S.at[mq * 4 + c], nd);
             C.slew[pin * 4 + c] = __dsqrt_rn(__dadd_rn(__dmul_rn(sr, sr), __dmul_rn(im, im)));
         }
-        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[qi * 2 + j], nd);
+        if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[mq * 2 + j], nd);
     }
     __syncthreads();                         // smem reusable by the next task
 }
