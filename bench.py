@@ -236,6 +236,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2603_28381_b200 as ws
     from paper_2603_28381_b200 import _lib
+    from paper_2603_28381_b200.corners import reduce_batch
 
     t0 = time.time()
     raw = G.generate_raw(cfg)
@@ -259,8 +260,6 @@ def main():
 
     # zero-copy torch views of the corner's results in HBM
     d_arc, d_edge, summ = dev.tensor("d_arc"), dev.tensor("d_edge"), dev.tensor("summary")
-    tl = torch.zeros(2, dtype=torch.float64, device="cuda")
-    idx = torch.tensor([0, 2], device="cuda")
 
     def step():
         dev.run(flags, stream=stream)
@@ -268,11 +267,7 @@ def main():
     def collectives():
         if world > 1:
             # the batch objective: TNS / loss SUM, WNS MIN, gradients SUM
-            torch.index_select(summ, 0, idx, out=tl)
-            dist.all_reduce(tl, op=dist.ReduceOp.SUM)
-            dist.all_reduce(summ[1:2], op=dist.ReduceOp.MIN)
-            dist.all_reduce(d_arc, op=dist.ReduceOp.SUM)
-            dist.all_reduce(d_edge, op=dist.ReduceOp.SUM)
+            reduce_batch(summ, d_arc, d_edge)
 
     for _ in range(max(3, args.warmup)):
         step()

@@ -1,0 +1,62 @@
+"""Corner / placement-candidate batches across GPUs.
+
+A single design does not shard (levels serialize), so the unit of
+distribution is a whole corner: corner k runs on rank k mod G, each rank
+running the full pass for its corners.  One exchange per batch step: the
+batch objective sum_k loss_k and TNS are SUM-reduced, WNS MIN-reduced, and
+the gradients d_arc / d_edge SUM-reduced (the gradient of the summed
+objective).  The tensors are the engine's zero-copy views, so the NCCL
+collectives run on the engine's stream right after the pass.
+
+The reference's only analog is its bench process pool (bench.py:188-191).
+"""
+
+from __future__ import annotations
+
+
+def corners_of_rank(n_corners: int, rank: int, world: int) -> list:
+    """Round-robin corner ownership: corner k on rank k mod world."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return [k for k in range(n_corners) if k % world == rank]
+
+
+def corner_scales(k: int):
+    """C5 corner k: res x (0.85 + 0.02k); caps and LUT
+    tables x (0.90 + 0.0125k)."""
+    return 0.85 + 0.02 * k, 0.90 + 0.0125 * k
+
+
+def corner_values(raw, k: int) -> dict:
+    fr, fc = corner_scales(k)
+    return dict(mem_res=raw.mem_res * fr, mem_cap=raw.mem_cap * fc, root_cap=raw.root_cap * fc,
+                lut_t_flat=raw.lut_t_flat * fc)
+
+
+def reduce_batch(summary, d_arc=None, d_edge=None, group=None):
+    """In-place batch reduction over the process group.
+
+    summary: fp64 tensor [3] = (TNS, WNS, loss) of this rank's corners (for
+    several local corners, pre-combine them with ``combine_local``).
+    TNS, loss: SUM; WNS: MIN; d_arc, d_edge: SUM."""
+    import torch
+    import torch.distributed as dist
+    sl = torch.stack([summary[0], summary[2]])
+    dist.all_reduce(sl, op=dist.ReduceOp.SUM, group=group)
+    wn = summary[1:2].clone()
+    dist.all_reduce(wn, op=dist.ReduceOp.MIN, group=group)
+    summary[0] = sl[0]
+    summary[2] = sl[1]
+    summary[1] = wn[0]
+    for g in (d_arc, d_edge):
+        if g is not None:
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
+    return summary
+
+
+def combine_local(summaries):
+    """(TNS, WNS, loss) of several corners on one rank -> one row, in corner
+    order (sum, min, sum)."""
+    import torch
+    s = torch.stack(list(summaries))
+    return torch.stack([s[:, 0].sum(), s[:, 1].min(), s[:, 2].sum()])

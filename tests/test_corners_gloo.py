@@ -1,0 +1,89 @@
+"""Multi-GPU host logic on CPU: world_size-2 gloo run of the corner-batch
+reduction (paper_2603_28381_b200/corners.py) used by bench.py --gpus N.
+
+Each rank owns its round-robin corners of a golden design, evaluates them
+with the oracle (the checker; the device path is covered by the gpu tests),
+and reduces (TNS, WNS, loss) and the gradients with ``reduce_batch``; rank 0
+compares against all corners evaluated serially.
+"""
+
+import copy
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_28381_b200 import corners as CO
+
+N_CORNERS = 4
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _corner_result(name, k):
+    from golden_util import load, raw_ns
+    from oracle import oracle as O
+    g = load(name)
+    ns = raw_ns(g)
+    base = O.flatten_raw(ns)
+    fl = copy.copy(base)
+    fr, fc = CO.corner_scales(k)
+    fl.mem_res = base.mem_res * fr
+    fl.mem_cap = base.mem_cap * fc
+    fl.root_cap = base.root_cap * fc
+    fl.lut_t_flat = base.lut_t_flat * fc
+    st = O.run_engine(fl)
+    gr = O.timing_gradients(fl, st, gamma=0.01 * ns.clock_period)
+    summ = torch.tensor([O.tns(st, fl), O.wns(st, fl), gr.loss], dtype=torch.float64)
+    return summ, torch.from_numpy(gr.d_arc.copy()), torch.from_numpy(gr.d_edge.copy())
+
+
+def _worker(rank, world, port, name, out):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        mine = CO.corners_of_rank(N_CORNERS, rank, world)
+        res = [_corner_result(name, k) for k in mine]
+        summ = CO.combine_local([r[0] for r in res])
+        d_arc = sum(r[1] for r in res)
+        d_edge = sum(r[2] for r in res)
+        CO.reduce_batch(summ, d_arc, d_edge)
+        if rank == 0:
+            torch.save({"summ": summ, "d_arc": d_arc, "d_edge": d_edge}, out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_corner_assignment_round_robin():
+    assert CO.corners_of_rank(16, 3, 8) == [3, 11]
+    allk = sorted(k for r in range(4) for k in CO.corners_of_rank(16, r, 4))
+    assert allk == list(range(16))
+    with pytest.raises(ValueError):
+        CO.corners_of_rank(4, 2, 2)
+
+
+@pytest.mark.parametrize("name", ["kat_chain5_viol", "gen_c1_star"])
+def test_gloo_world2_batch_reduction(tmp_path, name):
+    out = str(tmp_path / "r0.pt")
+    mp.spawn(_worker, args=(2, _free_port(), name, out), nprocs=2, join=True)
+    got = torch.load(out)
+    ref = [_corner_result(name, k) for k in range(N_CORNERS)]
+    exp = CO.combine_local([r[0] for r in ref])
+    # TNS / loss: sums of 2 partial sums vs a 4-term sum — fp64 reassociation only
+    np.testing.assert_allclose(got["summ"][[0, 2]].numpy(), exp[[0, 2]].numpy(), rtol=1e-12)
+    assert float(got["summ"][1]) == float(exp[1])                       # MIN is exact
+    np.testing.assert_allclose(got["d_arc"].numpy(), sum(r[1] for r in ref).numpy(), rtol=1e-12)
+    np.testing.assert_allclose(got["d_edge"].numpy(), sum(r[2] for r in ref).numpy(), rtol=1e-12)
