@@ -1190,6 +1190,24 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_tree(Topo t, Corners cs)
 }
 
 // ---- per-level kernels (one task per block; PDL prologue = records) --------
+#ifdef WS_PROBE
+// per-launch block timeline: 0 start | 1 records loaded | 2 PDL wait released | 3 end | 4 SM id
+#define LSTAMP(slot)                                                                          \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && t.probe) {                                                    \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[(size_t)blockIdx.x * 8 + (slot)] = _v;                                     \
+            if ((slot) == 0) {                                                                \
+                unsigned _sm;                                                                 \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(_sm));                              \
+                t.probe[(size_t)blockIdx.x * 8 + 4] = _sm;                                    \
+            }                                                                                 \
+        }                                                                                     \
+    } while (0)
+#else
+#define LSTAMP(slot) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w)
 {
@@ -1209,14 +1227,18 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_fwd(Topo t, LutSrc ls, Corners 
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ FwdSmem S;
     pdl_trigger();
+    LSTAMP(0);
     const Corner& C = cs.c[blockIdx.y];
     LutView L;
     if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
     const Task T = load_task(t, k0 + blockIdx.x);
     FwdRec R;
     fwd_records<HARD>(t, T, S, R);
+    LSTAMP(1);
     pdl_wait();          // the previous level's results are now visible
+    LSTAMP(2);
     fwd_body<HARD, LSE>(t, L, C, T, S, R, g);
+    LSTAMP(3);
 }
 
 template <bool HARD, bool GRAD>
@@ -1225,11 +1247,15 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_bwd(Topo t, Corners cs, int k0,
 {
     __shared__ BwdSmem S;
     pdl_trigger();
+    LSTAMP(0);
     const Task T = load_task(t, k0 + blockIdx.x);
     BwdRec R;
     bwd_records<GRAD>(t, T, S, R);
+    LSTAMP(1);
     pdl_wait();          // the next-higher level's results are now visible
+    LSTAMP(2);
     bwd_body<HARD, GRAD>(t, cs.c[blockIdx.y], T, S, R, g, kind, variant);
+    LSTAMP(3);
 }
 
 // pins finished after the level loop: pins in no net (seed + out-arcs) and
