@@ -74,7 +74,16 @@ typedef struct ws_ctx ws_ctx;
 /* per-corner value arrays (ws_set_values) */
 enum ws_value_field {
     WS_V_MEM_RES = 0, WS_V_MEM_CAP = 1, WS_V_ROOT_CAP = 2, WS_V_LUT_T = 3,
-    WS_V_PI_ARRIVAL = 4, WS_V_PI_SLEW = 5, WS_V_EP_REQUIRED = 6
+    WS_V_PI_ARRIVAL = 4, WS_V_PI_SLEW = 5, WS_V_EP_REQUIRED = 6,
+    /* position model (no reference counterpart: SURVEY.md §8(f) rank 1; the
+     * reference's gradients stop at d_arc / d_edge, diff.py:5-7).  Setting any
+     * of these enables it for every corner; until set, positions are 0, the
+     * base RC is the corner's RC and the wire coefficients are 0. */
+    WS_V_XY = 7,          /* [P*2] pin x, y */
+    WS_V_RES0 = 8,        /* [M*4] base resistance of each member edge */
+    WS_V_CAP0 = 9,        /* [M*4] base capacitance of each member edge */
+    WS_V_WIRE = 10        /* [8] r_unit[4], c_unit[4]: res = res0 + r_unit*len, cap = cap0 + c_unit*len,
+                             len = |dx| + |dy| between a member pin and its parent pin */
 };
 
 /* per-corner result arrays (ws_get / ws_device_ptr); float64 */
@@ -83,7 +92,13 @@ enum ws_state_field {
     WS_F_REQUIRED = 5, WS_F_SLACK = 6, WS_F_ARC_DELAY = 7,             /* (P,4) / (A,4) */
     WS_F_LSE_ARRIVAL = 8, WS_F_ARC_WEIGHTS = 9, WS_F_D_ARC = 10,       /* (P,2) (A,2) (A,2) */
     WS_F_D_EDGE = 11, WS_F_ADJOINT = 12,                               /* (M,2) (P,2) */
-    WS_F_SUMMARY = 13                                                  /* (3,) TNS WNS loss */
+    WS_F_SUMMARY = 13,                                                 /* (3,) TNS WNS loss */
+    /* position gradients (late cols; WS_RUN_POSGRAD) */
+    WS_F_D_RES = 14, WS_F_D_CAP = 15,   /* (M,2) dL/dmem_res, dL/dmem_cap */
+    WS_F_D_ROOT_CAP = 16,               /* (N,2) dL/droot_cap (= dL/dload of the root) */
+    WS_F_D_SLEW = 17,                   /* (P,2) dL/dslew */
+    WS_F_D_LEN = 18,                    /* (M,)  dL/dlength of each member edge */
+    WS_F_D_XY = 19                      /* (P,2) dL/dx, dL/dy */
 };
 
 /* topology arrays (ws_get_topology); int64 on the host like FlatDesign */
@@ -109,8 +124,11 @@ enum ws_run_flags {
     WS_RUN_GRAPH = 32u,      /* capture the pass into a CUDA graph once, replay afterwards */
     WS_RUN_SUMMARY = 64u,    /* TNS/WNS (sta.py:408-421) from the corner's current slack */
     WS_RUN_SLACK = 128u,     /* slack (warp.py:474-475) from the current arrival/required */
-    WS_RUN_PERSISTENT = 256u /* with HARD (and LSE|GRAD): the whole pass as one cooperative
+    WS_RUN_PERSISTENT = 256u,/* with HARD (and LSE|GRAD): the whole pass as one cooperative
                                 kernel, grid barrier between levels */
+    WS_RUN_WIRE = 512u,      /* first: mem_res / mem_cap from the positions (WS_V_XY ...) */
+    WS_RUN_POSGRAD = 1024u   /* last (needs HARD|LSE|GRAD in the same call): slew / load
+                                adjoint sweep, Elmore adjoint, dL/dxy */
 };
 
 enum ws_loss_kind { WS_LOSS_HINGE = 0, WS_LOSS_SOFTPLUS = 1 };

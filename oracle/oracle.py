@@ -264,3 +264,102 @@ def interpolate(flat, lut, qs, ql):
     return lib().orc_interp(ctypes.c_int64(lut), _p(flat.lut_s_ptr), _p(flat.lut_l_ptr),
                             _p(flat.lut_t_ptr), _p(flat.lut_s_flat), _p(flat.lut_l_flat),
                             _p(flat.lut_t_flat), ctypes.c_double(qs), ctypes.c_double(ql))
+
+
+# ---------------------------------------------------------------------------
+# Position model + position gradients.  The reference
+# has no position model (SPEC.md: pin-location gradients are a non-goal), so
+# these are this repo's definitions, pinned by central finite differences of
+# the reference-restated loss (tests/test_place_oracle.py).
+
+def parent_pins(flat):
+    """Parent pin of every member: the net root for depth 0, else the parent
+    member's pin (mem_parent_loc, flatten.py:198-203)."""
+    M = len(flat.mem_pin)
+    if M == 0:
+        return np.zeros(0, np.int64)
+    pl = flat.mem_parent_loc
+    root = flat.net_root[flat.mem_net]
+    s = flat.net_ptr[flat.mem_net]
+    par = np.where(pl > 0, flat.mem_pin[np.maximum(s + pl - 1, 0)], root)
+    return np.ascontiguousarray(par, dtype=np.int64)
+
+
+def pin_out(flat):
+    """Arcs grouped by source pin, ascending arc id (CSR over all pins)."""
+    P = flat.n_pins
+    order = np.argsort(flat.arc_from, kind="stable").astype(np.int64)
+    ptr = np.zeros(P + 1, np.int64)
+    np.add.at(ptr, flat.arc_from + 1, 1)
+    return np.cumsum(ptr), order
+
+
+def wire(flat, xy, res0, cap0, r_unit, c_unit):
+    """mem_res / mem_cap of the Manhattan wire model (orc_wire)."""
+    M = len(flat.mem_pin)
+    res, cap = np.zeros((M, 4)), np.zeros((M, 4))
+    lib().orc_wire(ctypes.c_int64(M), _p(_i64(flat.mem_pin)), _p(parent_pins(flat)), _p(_f64(xy)),
+                   _p(_f64(res0)), _p(_f64(cap0)), _p(_f64(r_unit)), _p(_f64(c_unit)), _p(res),
+                   _p(cap))
+    return res, cap
+
+
+def with_values(flat, **arrays):
+    """copy.copy(flat) with value arrays substituted."""
+    import copy
+    f = copy.copy(flat)
+    for k, v in arrays.items():
+        setattr(f, k, np.ascontiguousarray(v, dtype=np.float64))
+    return f
+
+
+def placed_loss(flat, xy, res0, cap0, r_unit, c_unit, gamma, loss="hinge"):
+    """positions -> wire RC -> run_engine -> timing_gradients loss."""
+    res, cap = wire(flat, xy, res0, cap0, r_unit, c_unit)
+    f = with_values(flat, mem_res=res, mem_cap=cap)
+    st = run_engine(f)
+    return timing_gradients(f, st, gamma=gamma, loss=loss).loss
+
+
+def interp_grad(flat, lut, qs, ql):
+    out = np.zeros(2)
+    lib().orc_interp_grad(ctypes.c_int64(lut), _p(flat.lut_s_ptr), _p(flat.lut_l_ptr),
+                          _p(flat.lut_t_ptr), _p(flat.lut_s_flat), _p(flat.lut_l_flat),
+                          _p(flat.lut_t_flat), ctypes.c_double(qs), ctypes.c_double(ql), _p(out))
+    return out
+
+
+def position_gradients(flat, st, gr, xy=None, r_unit=None, c_unit=None):
+    """Reverse sweep of orc_posgrad_level over the levels (descending), then
+    orc_pos_reduce when positions are given.  flat must hold the RC values the
+    state was computed with."""
+    L = lib()
+    P, A, M, N = flat.n_pins, flat.n_arcs, len(flat.mem_pin), len(flat.net_root)
+    po_ptr, po_arc = pin_out(flat)
+    gs, gsr, gsa = np.zeros((P, 2)), np.zeros((P, 2)), np.zeros((A, 2))
+    gl = np.zeros((N, 2))
+    d_res, d_cap, d_root_cap = np.zeros((M, 2)), np.zeros((M, 2)), np.zeros((N, 2))
+    mx = int(flat.net_m.max()) if N else 1
+    scratch = np.zeros(3 * max(1, mx))
+    adj = np.ascontiguousarray(gr.adjoint)
+    d_arc = np.ascontiguousarray(gr.d_arc)
+    for li in range(flat.n_levels - 1, -1, -1):
+        nets = _i64(flat.levels[li])
+        L.orc_posgrad_level(
+            ctypes.c_int64(len(nets)), _p(nets), _p(flat.net_ptr), _p(flat.net_root),
+            _p(flat.root_kind), _p(flat.mem_pin), _p(flat.mem_parent_loc), _p(flat.net_in_ptr),
+            _p(flat.net_in_arc), _p(flat.arc_from), _p(flat.arc_dlut), _p(flat.arc_slut),
+            _p(po_ptr), _p(po_arc), _p(flat.root_net_of_pin), _p(flat.lut_s_ptr),
+            _p(flat.lut_l_ptr), _p(flat.lut_t_ptr), _p(flat.lut_s_flat), _p(flat.lut_l_flat),
+            _p(flat.lut_t_flat), _p(flat.mem_res), _p(flat.mem_cap), _p(st.load),
+            _p(st.net_delay), _p(st.impulse), _p(st.slew), _p(st.arrival), _p(st.arc_delay),
+            _p(adj), _p(d_arc), _p(gs), _p(gsr), _p(gsa), _p(gl), _p(d_res), _p(d_cap),
+            _p(d_root_cap), _p(scratch))
+    out = SimpleNamespace(d_slew=gs, d_load=gl, d_res=d_res, d_cap=d_cap, d_root_cap=d_root_cap)
+    if xy is not None:
+        g_len, dxy = np.zeros(M), np.zeros((P, 2))
+        L.orc_pos_reduce(ctypes.c_int64(M), _p(_i64(flat.mem_pin)), _p(parent_pins(flat)),
+                         _p(_f64(xy)), _p(_f64(r_unit)), _p(_f64(c_unit)), _p(d_res), _p(d_cap),
+                         _p(g_len), _p(dxy))
+        out.g_len, out.d_xy = g_len, dxy
+    return out

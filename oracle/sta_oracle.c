@@ -447,3 +447,229 @@ void orc_grad_level(i64 n_lv, const i64 *nets, const i64 *net_ptr, const i64 *ne
             }
         }
 }
+
+/* ------------------------------------------------------------------ */
+/* Position model and position gradients (north_star: "gradients w.r.t.
+ * pin/cell positions").  The reference stops at
+ * delay-space gradients (diff.py:5-7; SPEC.md "Non-goals: pin-location
+ * gradients"), so this part has no reference routine to restate: it is the
+ * exact reverse-mode derivative of the reference's own forward functions
+ * (rc_level _kernels.pyx:84-156, _interp :15-81, forward_level :159-210,
+ * _lse_forward_level diff.py:123-146) composed with a Manhattan wire model,
+ * and it is pinned by central finite differences of the reference-restated
+ * loss (tests/test_place_oracle.py) — "parity pinned by FD", not by golden
+ * vectors.
+ *
+ * Wire model: member k of a net, parent pin q (the root for depth 0, else
+ * its parent member), length l_k = |x_k - x_q| + |y_k - y_q|;
+ *   mem_res[k,c] = res0[k,c] + r_unit[c] * l_k
+ *   mem_cap[k,c] = cap0[k,c] + c_unit[c] * l_k                               */
+
+void orc_wire(i64 M, const i64 *mem_pin, const i64 *parent_pin, const double *xy,
+              const double *res0, const double *cap0, const double *ru, const double *cu,
+              double *res, double *cap)
+{
+    for (i64 k = 0; k < M; k++) {
+        i64 p = mem_pin[k], q = parent_pin[k];
+        double l = fabs(xy[p * 2] - xy[q * 2]) + fabs(xy[p * 2 + 1] - xy[q * 2 + 1]);
+        for (int c = 0; c < 4; c++) {
+            res[k * 4 + c] = res0[k * 4 + c] + ru[c] * l;
+            cap[k * 4 + c] = cap0[k * 4 + c] + cu[c] * l;
+        }
+    }
+}
+
+/* d out / d qs and d out / d ql of _interp (_kernels.pyx:15-81): the partial
+ * derivatives of the bilinear form inside the located cell; 0 along an axis
+ * whose fraction was clamped (query outside the table) or with one point. */
+static void interp_grad(i64 lut, const i64 *s_ptr, const i64 *l_ptr, const i64 *t_ptr,
+                        const double *s_flat, const double *l_flat, const double *t_flat,
+                        double qs, double ql, double *ds, double *dl)
+{
+    i64 s0 = s_ptr[lut], nS = s_ptr[lut + 1] - s0;
+    i64 l0 = l_ptr[lut], nL = l_ptr[lut + 1] - l0;
+    i64 t0 = t_ptr[lut];
+    i64 lo, hi, mid, si, li, si2, li2;
+    double st, lt, hs = 0.0, hl = 0.0;
+    int fs = 0, fl = 0;
+    if (nS > 1) {
+        lo = 0; hi = nS;
+        while (lo < hi) { mid = (lo + hi) / 2; if (s_flat[s0 + mid] <= qs) lo = mid + 1; else hi = mid; }
+        si = lo - 1;
+        if (si < 0) si = 0; else if (si > nS - 2) si = nS - 2;
+        hs = s_flat[s0 + si + 1] - s_flat[s0 + si];
+        st = (qs - s_flat[s0 + si]) / hs;
+        if (st < 0.0) st = 0.0; else if (st > 1.0) st = 1.0; else fs = 1;
+        si2 = si + 1;
+    } else { si = 0; st = 0.0; si2 = 0; }
+    if (nL > 1) {
+        lo = 0; hi = nL;
+        while (lo < hi) { mid = (lo + hi) / 2; if (l_flat[l0 + mid] <= ql) lo = mid + 1; else hi = mid; }
+        li = lo - 1;
+        if (li < 0) li = 0; else if (li > nL - 2) li = nL - 2;
+        hl = l_flat[l0 + li + 1] - l_flat[l0 + li];
+        lt = (ql - l_flat[l0 + li]) / hl;
+        if (lt < 0.0) lt = 0.0; else if (lt > 1.0) lt = 1.0; else fl = 1;
+        li2 = li + 1;
+    } else { li = 0; lt = 0.0; li2 = 0; }
+    double t00 = t_flat[t0 + si * nL + li], t01 = t_flat[t0 + si * nL + li2];
+    double t10 = t_flat[t0 + si2 * nL + li], t11 = t_flat[t0 + si2 * nL + li2];
+    double v0 = (1.0 - lt) * t00 + lt * t01;
+    double v1 = (1.0 - lt) * t10 + lt * t11;
+    *ds = fs ? (v1 - v0) / hs : 0.0;
+    *dl = fl ? ((1.0 - st) * (t01 - t00) + st * (t11 - t10)) / hl : 0.0;
+}
+
+void orc_interp_grad(i64 lut, const i64 *s_ptr, const i64 *l_ptr, const i64 *t_ptr,
+                     const double *s_flat, const double *l_flat, const double *t_flat,
+                     double qs, double ql, double *out2)
+{
+    interp_grad(lut, s_ptr, l_ptr, t_ptr, s_flat, l_flat, t_flat, qs, ql, out2, out2 + 1);
+}
+
+/* One level of the reverse sweep (levels descending), late conditions only
+ * (the loss sees only lse_arrival, diff.py:21).  With adj = dL/dlse_at (the
+ * GradientState adjoint) and d_arc = dL/darc_delay:
+ *   gs[p]   = dL/dslew[p]  = sum over out-arcs a of gsa[a]
+ *                            (+ gsr[p] when p roots a feedthrough net)
+ *   gsa[a]  = d_arc[a] dD_a/dslew + [a wins its root] gs[root] dS_a/dslew
+ *   gsr[r]  = sum over members m of gs[m] slew[r] / slew[m]   (slew = sqrt(sr^2 + imp^2))
+ *   gl[n]   = dL/dload[root] = sum_a d_arc[a] dD_a/dload + gs[root] dS_w/dload
+ * then the Elmore adjoint of the net (rc_level order: buf = downstream caps,
+ * d = cumulative delay, imp = sqrt(2 r cap d - d^2)):
+ *   A_k = adj[m_k] + gimp_k (r_k cap_k - d_k) / imp_k,  gimp_k = gs[m_k] imp_k / slew[m_k]
+ *   D_k = A_k + sum over children D_child
+ *   d_res[k] = D_k buf_k + gimp_k cap_k d_k / imp_k
+ *   B_k = D_k r_k + gl[n] + B_parent(k)      (load[root] = root_cap + sum_k buf_k)
+ *   d_cap[k] = B_k + gimp_k r_k d_k / imp_k,  d_root_cap[n] = gl[n]
+ * scratch: 3 * max members doubles. */
+void orc_posgrad_level(i64 n_lv, const i64 *nets, const i64 *net_ptr, const i64 *net_root,
+                       const i64 *root_kind, const i64 *mem_pin, const i64 *mem_parent_loc,
+                       const i64 *net_in_ptr, const i64 *net_in_arc, const i64 *arc_from,
+                       const i64 *arc_dlut, const i64 *arc_slut, const i64 *pin_out_ptr,
+                       const i64 *pin_out_arc, const i64 *root_net_of_pin,
+                       const i64 *s_ptr, const i64 *l_ptr, const i64 *t_ptr,
+                       const double *s_flat, const double *l_flat, const double *t_flat,
+                       const double *mem_res, const double *mem_cap, const double *load,
+                       const double *net_delay, const double *impulse, const double *slew,
+                       const double *arrival, const double *arc_delay, const double *adj,
+                       const double *d_arc, double *gs, double *gsr, double *gsa, double *gl_out,
+                       double *d_res, double *d_cap, double *d_root_cap, double *scratch)
+{
+    for (i64 ni = 0; ni < n_lv; ni++) {
+        i64 net = nets[ni], s = net_ptr[net], e = net_ptr[net + 1], m = e - s, root = net_root[net];
+        double *gimp = scratch, *buf = scratch + m, *acc = scratch + 2 * m;
+        for (int j = 0; j < 2; j++) {
+            int c = 2 + j;
+            double sr = slew[root * 4 + c], gsum = 0.0, gl = 0.0;
+            for (i64 k = s; k < e; k++) {
+                i64 pin = mem_pin[k];
+                double g = 0.0;
+                for (i64 t = pin_out_ptr[pin]; t < pin_out_ptr[pin + 1]; t++)
+                    g += gsa[pin_out_arc[t] * 2 + j];
+                if (root_net_of_pin[pin] >= 0) g += gsr[pin * 2 + j];
+                gs[pin * 2 + j] = g;
+                double sm = slew[pin * 4 + c];
+                if (sm > 0.0) {
+                    gsum += g * (sr / sm);
+                    gimp[k - s] = g * (impulse[pin * 4 + c] / sm);
+                } else {
+                    gimp[k - s] = 0.0;
+                }
+            }
+            if (root_kind[net] == 2) {
+                gsr[root * 2 + j] = gsum;          /* the parent net's member loop adds it */
+            } else {
+                double groot = gsum;
+                for (i64 t = pin_out_ptr[root]; t < pin_out_ptr[root + 1]; t++)
+                    groot += gsa[pin_out_arc[t] * 2 + j];
+                gs[root * 2 + j] = groot;
+                if (root_kind[net] == 0) {
+                    double ld = load[root * 4 + c], best = -INFINITY;
+                    i64 w = -1;
+                    for (i64 t = net_in_ptr[net]; t < net_in_ptr[net + 1]; t++) {
+                        i64 a = net_in_arc[t];
+                        double v = arrival[arc_from[a] * 4 + c] + arc_delay[a * 4 + c];
+                        if (v > best) { best = v; w = a; }
+                    }
+                    for (i64 t = net_in_ptr[net]; t < net_in_ptr[net + 1]; t++) {
+                        i64 a = net_in_arc[t];
+                        double ds, dl;
+                        interp_grad(arc_dlut[a * 4 + c], s_ptr, l_ptr, t_ptr, s_flat, l_flat, t_flat,
+                                    slew[arc_from[a] * 4 + c], ld, &ds, &dl);
+                        gsa[a * 2 + j] = d_arc[a * 2 + j] * ds;
+                        gl += d_arc[a * 2 + j] * dl;
+                    }
+                    if (w >= 0) {
+                        double ds, dl;
+                        interp_grad(arc_slut[w * 4 + c], s_ptr, l_ptr, t_ptr, s_flat, l_flat, t_flat,
+                                    slew[arc_from[w] * 4 + c], ld, &ds, &dl);
+                        gsa[w * 2 + j] += groot * ds;
+                        gl += groot * dl;
+                    }
+                }
+            }
+            gl_out[net * 2 + j] = gl;
+            d_root_cap[net * 2 + j] = gl;
+            /* Elmore adjoint */
+            for (i64 k = 0; k < m; k++) buf[k] = mem_cap[(s + k) * 4 + c];
+            for (i64 k = m - 1; k > 0; k--) {
+                i64 pl = mem_parent_loc[s + k];
+                if (pl > 0) buf[pl - 1] += buf[k];
+            }
+            for (i64 k = 0; k < m; k++) {
+                i64 pin = mem_pin[s + k];
+                double r = mem_res[(s + k) * 4 + c], cp = mem_cap[(s + k) * 4 + c];
+                double d = net_delay[pin * 4 + c], im = impulse[pin * 4 + c];
+                acc[k] = adj[pin * 2 + j];
+                if (im > 0.0) acc[k] += gimp[k] * ((r * cp - d) / im);
+            }
+            for (i64 k = m - 1; k > 0; k--) {
+                i64 pl = mem_parent_loc[s + k];
+                if (pl > 0) acc[pl - 1] += acc[k];
+            }
+            for (i64 k = 0; k < m; k++) {
+                i64 pin = mem_pin[s + k];
+                double r = mem_res[(s + k) * 4 + c], cp = mem_cap[(s + k) * 4 + c];
+                double d = net_delay[pin * 4 + c], im = impulse[pin * 4 + c];
+                double dr = acc[k] * buf[k];
+                if (im > 0.0) dr += gimp[k] * ((cp * d) / im);
+                d_res[(s + k) * 2 + j] = dr;
+                acc[k] = acc[k] * r + gl;          /* acc now holds B_k (direct part) */
+            }
+            for (i64 k = 1; k < m; k++) {
+                i64 pl = mem_parent_loc[s + k];
+                if (pl > 0) acc[k] += acc[pl - 1];
+            }
+            for (i64 k = 0; k < m; k++) {
+                i64 pin = mem_pin[s + k];
+                double r = mem_res[(s + k) * 4 + c];
+                double d = net_delay[pin * 4 + c], im = impulse[pin * 4 + c];
+                double dc = acc[k];
+                if (im > 0.0) dc += gimp[k] * ((r * d) / im);
+                d_cap[(s + k) * 2 + j] = dc;
+            }
+        }
+    }
+}
+
+/* dL/dl_k = sum_j d_res[k,j] r_unit[2+j] + d_cap[k,j] c_unit[2+j], then
+ * dL/dx: +dL/dl_k sign(x_k - x_q) on the member pin, minus it on the parent
+ * pin q (sign(0) = 0); y likewise.  dxy (P,2) must be zeroed. */
+void orc_pos_reduce(i64 M, const i64 *mem_pin, const i64 *parent_pin, const double *xy,
+                    const double *ru, const double *cu, const double *d_res, const double *d_cap,
+                    double *g_len, double *dxy)
+{
+    for (i64 k = 0; k < M; k++) {
+        double g = 0.0;
+        for (int j = 0; j < 2; j++) g += d_res[k * 2 + j] * ru[2 + j] + d_cap[k * 2 + j] * cu[2 + j];
+        g_len[k] = g;
+        i64 p = mem_pin[k], q = parent_pin[k];
+        for (int a = 0; a < 2; a++) {
+            double dd = xy[p * 2 + a] - xy[q * 2 + a];
+            double sg = dd > 0.0 ? 1.0 : (dd < 0.0 ? -1.0 : 0.0);
+            dxy[p * 2 + a] += g * sg;
+            dxy[q * 2 + a] -= g * sg;
+        }
+    }
+}

@@ -20,17 +20,22 @@ WS_OK, WS_ERR_VALUE, WS_ERR_CYCLE, WS_ERR_NOMEM, WS_ERR_CUDA, WS_ERR_STATE = ran
 
 # value fields
 V_MEM_RES, V_MEM_CAP, V_ROOT_CAP, V_LUT_T, V_PI_ARRIVAL, V_PI_SLEW, V_EP_REQUIRED = range(7)
+V_XY, V_RES0, V_CAP0, V_WIRE = range(7, 11)
 # state fields
 (F_LOAD, F_NET_DELAY, F_IMPULSE, F_SLEW, F_ARRIVAL, F_REQUIRED, F_SLACK, F_ARC_DELAY,
  F_LSE_ARRIVAL, F_ARC_WEIGHTS, F_D_ARC, F_D_EDGE, F_ADJOINT, F_SUMMARY) = range(14)
+F_D_RES, F_D_CAP, F_D_ROOT_CAP, F_D_SLEW, F_D_LEN, F_D_XY = range(14, 20)
 STATE_FIELDS = {"load": F_LOAD, "net_delay": F_NET_DELAY, "impulse": F_IMPULSE, "slew": F_SLEW,
                 "arrival": F_ARRIVAL, "required": F_REQUIRED, "slack": F_SLACK,
                 "arc_delay": F_ARC_DELAY, "lse_arrival": F_LSE_ARRIVAL,
                 "arc_weights": F_ARC_WEIGHTS, "d_arc": F_D_ARC, "d_edge": F_D_EDGE,
-                "adjoint": F_ADJOINT, "summary": F_SUMMARY}
+                "adjoint": F_ADJOINT, "summary": F_SUMMARY,
+                "d_res": F_D_RES, "d_cap": F_D_CAP, "d_root_cap": F_D_ROOT_CAP,
+                "d_slew": F_D_SLEW, "d_len": F_D_LEN, "d_xy": F_D_XY}
 VALUE_FIELDS = {"mem_res": V_MEM_RES, "mem_cap": V_MEM_CAP, "root_cap": V_ROOT_CAP,
                 "lut_t_flat": V_LUT_T, "pi_arrival": V_PI_ARRIVAL, "pi_slew": V_PI_SLEW,
-                "ep_required": V_EP_REQUIRED}
+                "ep_required": V_EP_REQUIRED, "xy": V_XY, "res0": V_RES0, "cap0": V_CAP0,
+                "wire": V_WIRE}
 TOPO_FIELDS = ("net_ptr", "net_root", "root_kind", "mem_pin", "mem_parent_loc", "mem_net",
                "mem_local", "arc_from", "arc_to", "arc_dlut", "arc_slut", "net_in_ptr",
                "net_in_arc", "mem_out_ptr", "mem_out_arc", "net_m", "net_a", "net_o",
@@ -41,6 +46,7 @@ TOPO = {name: i for i, name in enumerate(TOPO_FIELDS)}
 RUN_HARD, RUN_LSE, RUN_GRAD, RUN_TWO_STREAM, RUN_FUSED, RUN_GRAPH, RUN_SUMMARY, RUN_SLACK = (
     1, 2, 4, 8, 16, 32, 64, 128)
 RUN_PERSISTENT = 256
+RUN_WIRE, RUN_POSGRAD = 512, 1024
 LOSS_KINDS = {"hinge": 0, "softplus": 1}
 DIMS_LEN = 11
 

@@ -53,12 +53,28 @@ int64_t value_len(const ws::Context& c, int field)
     case WS_V_LUT_T: return c.lut_t_len;
     case WS_V_PI_ARRIVAL: case WS_V_PI_SLEW: return 4ll * t.I;
     case WS_V_EP_REQUIRED: return 4ll * t.E;
+    case WS_V_XY: return 2ll * t.P;
+    case WS_V_RES0: case WS_V_CAP0: return 4ll * t.M;
+    case WS_V_WIRE: return 8;
     default: throw ws::Error(WS_ERR_VALUE, "unknown value field");
     }
 }
 
-double* value_ptr(ws::Corner& d, int field)
+bool place_field(int field) { return field >= WS_V_XY && field <= WS_V_WIRE; }
+
+double* value_ptr(ws::Context& c, int corner, int field)
 {
+    if (place_field(field)) {
+        ws::place_enable(c);
+        ws::PlaceCorner& g = c.place[corner];
+        switch (field) {
+        case WS_V_XY: return g.xy;
+        case WS_V_RES0: return g.res0;
+        case WS_V_CAP0: return g.cap0;
+        default: return g.wire;
+        }
+    }
+    ws::Corner& d = c.corners[corner].d;
     switch (field) {
     case WS_V_MEM_RES: return d.mem_res;
     case WS_V_MEM_CAP: return d.mem_cap;
@@ -82,12 +98,29 @@ int64_t state_len(const ws::Context& c, int field)
     case WS_F_ARC_WEIGHTS: case WS_F_D_ARC: return 2ll * t.A;
     case WS_F_D_EDGE: return 2ll * t.M;
     case WS_F_SUMMARY: return 3;
+    case WS_F_D_RES: case WS_F_D_CAP: return 2ll * t.M;
+    case WS_F_D_ROOT_CAP: return 2ll * t.N;
+    case WS_F_D_SLEW: case WS_F_D_XY: return 2ll * t.P;
+    case WS_F_D_LEN: return t.M;
     default: throw ws::Error(WS_ERR_VALUE, "unknown state field");
     }
 }
 
-double* state_ptr(ws::Corner& d, int field)
+double* state_ptr(ws::Context& c, int corner, int field)
 {
+    if (field >= WS_F_D_RES && field <= WS_F_D_XY) {
+        ws::place_enable(c);
+        ws::PlaceCorner& g = c.place[corner];
+        switch (field) {
+        case WS_F_D_RES: return g.d_res;
+        case WS_F_D_CAP: return g.d_cap;
+        case WS_F_D_ROOT_CAP: return g.d_root_cap;
+        case WS_F_D_SLEW: return g.gs;
+        case WS_F_D_LEN: return g.g_len;
+        default: return g.d_xy;
+        }
+    }
+    ws::Corner& d = c.corners[corner].d;
     switch (field) {
     case WS_F_LOAD: return d.load;
     case WS_F_NET_DELAY: return d.net_delay;
@@ -287,7 +320,7 @@ int ws_set_values(ws_ctx* h, int corner, int field, const double* src, int src_o
         const int64_t n = value_len(c, field);
         cudaStream_t s = as_stream(stream, c.s_main);
         if (n)
-            WS_CUDA(cudaMemcpyAsync(value_ptr(c.corners[corner].d, field), src, (size_t)n * sizeof(double),
+            WS_CUDA(cudaMemcpyAsync(value_ptr(c, corner, field), src, (size_t)n * sizeof(double),
                                     src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         if (!stream) WS_CUDA(cudaStreamSynchronize(s));
     });
@@ -336,6 +369,12 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
         if (granularity < 1) throw ws::Error(WS_ERR_VALUE, "granularity must be >= 1");
         cudaStream_t s = as_stream(stream, c.s_main);
         cudaStream_t g = as_stream(stream_grad, c.s_grad);
+        const unsigned need = WS_RUN_HARD | WS_RUN_LSE | WS_RUN_GRAD;
+        if ((flags & WS_RUN_POSGRAD) && (flags & need) != need)
+            throw ws::Error(WS_ERR_STATE, "WS_RUN_POSGRAD needs HARD|LSE|GRAD in the same run");
+        if ((flags & WS_RUN_POSGRAD) && (flags & WS_RUN_PERSISTENT))
+            throw ws::Error(WS_ERR_VALUE, "WS_RUN_POSGRAD is not available with WS_RUN_PERSISTENT");
+        if (flags & (WS_RUN_WIRE | WS_RUN_POSGRAD)) ws::place_enable(c);
         if (flags & WS_RUN_GRAPH) {
             const unsigned key = flags & ~WS_RUN_GRAPH;
             cudaGraphExec_t exec = nullptr;
@@ -386,7 +425,7 @@ int ws_set_state(ws_ctx* h, int corner, int field, const double* src, int src_on
         const int64_t n = state_len(c, field);
         cudaStream_t s = as_stream(stream, c.s_main);
         if (n)
-            WS_CUDA(cudaMemcpyAsync(state_ptr(c.corners[corner].d, field), src, (size_t)n * sizeof(double),
+            WS_CUDA(cudaMemcpyAsync(state_ptr(c, corner, field), src, (size_t)n * sizeof(double),
                                     src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         if (!stream) WS_CUDA(cudaStreamSynchronize(s));
     });
@@ -401,7 +440,7 @@ int ws_get(ws_ctx* h, int corner, int field, double* dst, int dst_on_device, voi
         const int64_t n = state_len(c, field);
         cudaStream_t s = as_stream(stream, c.s_main);
         if (n)
-            WS_CUDA(cudaMemcpyAsync(dst, state_ptr(c.corners[corner].d, field), (size_t)n * sizeof(double),
+            WS_CUDA(cudaMemcpyAsync(dst, state_ptr(c, corner, field), (size_t)n * sizeof(double),
                                     dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
         WS_CUDA(cudaStreamSynchronize(s));
     });
@@ -413,7 +452,7 @@ int ws_device_ptr(ws_ctx* h, int corner, int field, void** dptr, int64_t* n_elem
         if (!h || !dptr) throw ws::Error(WS_ERR_VALUE, "null argument");
         ws::Context& c = h->c;
         check_corner(c, corner);
-        *dptr = state_ptr(c.corners[corner].d, field);
+        *dptr = state_ptr(c, corner, field);
         if (n_elems) *n_elems = state_len(c, field);
     });
 }
@@ -424,7 +463,7 @@ int ws_value_ptr(ws_ctx* h, int corner, int field, void** dptr, int64_t* n_elems
         if (!h || !dptr) throw ws::Error(WS_ERR_VALUE, "null argument");
         ws::Context& c = h->c;
         check_corner(c, corner);
-        *dptr = value_ptr(c.corners[corner].d, field);
+        *dptr = value_ptr(c, corner, field);
         if (n_elems) *n_elems = value_len(c, field);
     });
 }

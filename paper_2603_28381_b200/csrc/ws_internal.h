@@ -78,6 +78,29 @@ struct SumPlan {
     int max_height = 0;
 };
 
+// position model (ws_place.cu): topology extras, built on first use
+struct PlaceTopo {
+    int* parent_pin = nullptr;   // [M] parent pin of each member edge
+    int* pc_ptr = nullptr;       // [P+1] member edges whose parent is the pin
+    int* pc_mem = nullptr;       // [M]   (ascending member index)
+    bool ready = false;
+};
+
+// per corner: positions, wire model, gradients (late cols) and scratch
+struct PlaceCorner {
+    double* xy = nullptr;        // (P,2) pin coordinates
+    double *res0 = nullptr, *cap0 = nullptr;   // (M,4) base RC of each member edge
+    double* wire = nullptr;      // [8] r_unit[4], c_unit[4]
+    double *gs = nullptr, *gsr = nullptr;      // (P,2) dL/dslew, feedthrough-root partials
+    double* gsa = nullptr;       // (A,2) slew adjoint an arc sends to its source pin
+    double* gl = nullptr;        // (N,2) dL/dload[root]
+    double *d_res = nullptr, *d_cap = nullptr; // (M,2)
+    double* d_root_cap = nullptr;  // (N,2)
+    double* g_len = nullptr;     // (M)   dL/dlength
+    double* d_xy = nullptr;      // (P,2)
+    double *sc_gimp = nullptr, *sc_buf = nullptr, *sc_acc = nullptr;   // (M,2) scratch
+};
+
 struct CornerSlot {
     Corner d;                  // device pointers
     bool has_lse = false;      // LSE forward done since the last hard pass
@@ -108,6 +131,8 @@ struct Context {
     struct GraphEntry { unsigned key; int c0, nc; double gamma; int loss; int gran; cudaGraphExec_t exec; };
     std::vector<GraphEntry> graphs;
     std::vector<int> graph_launches;  // kernels per captured graph
+    PlaceTopo pt;
+    std::vector<PlaceCorner> place;   // per corner once place_enable ran
 };
 
 void build_topology(Context& ctx, const ws_design_desc* d);
@@ -122,6 +147,9 @@ void launch_fwd_list(const Topo& t, const Corner* dcs, int n, int lut_s_len, int
 void launch_bwd_list(const Topo& t, const Corner* dcs, int n, cudaStream_t s);
 void launch_perturb(const Context& ctx, int dst, int src, unsigned long long seed, double sigma,
                     cudaStream_t s);
+void place_enable(Context& ctx);
+int launch_wire(Context& ctx, int c0, int nc, cudaStream_t s);
+int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s);
 void summary_plan_init(Context& ctx);
 void summary_plan_free(Context& ctx);
 void topo_field_to_host(Context& ctx, int field, int64_t* dst);

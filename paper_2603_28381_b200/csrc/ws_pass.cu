@@ -39,6 +39,10 @@
 
 namespace ws {
 
+#ifndef WS_MINB
+#define WS_MINB 2   // min resident blocks per SM of the level kernels
+#endif
+
 constexpr int MAXC = 16;   // corners per launch (blockIdx.y)
 struct Corners {
     Corner c[MAXC];
@@ -1221,7 +1225,7 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w)
 }
 
 template <bool HARD, bool LSE>
-__global__ void __launch_bounds__(PASS_TPB, 2) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
+__global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
                                                      bool use_smem, double g)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1242,7 +1246,7 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_fwd(Topo t, LutSrc ls, Corners 
 }
 
 template <bool HARD, bool GRAD>
-__global__ void __launch_bounds__(PASS_TPB, 2) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
+__global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
                                                      int variant)
 {
     __shared__ BwdSmem S;
@@ -1970,9 +1974,11 @@ void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int lo
               int granularity, cudaStream_t s, cudaStream_t gs, int w)
 {
     int count = 0;
+    if (flags & WS_RUN_WIRE) count += launch_wire(ctx, c0, nc, s);
     for (int k = 0; k < nc; k += MAXC)
         run_chunk(ctx, c0 + k, std::min(MAXC, nc - k), flags, gamma, loss_kind, granularity, s, gs,
                   w, count);
+    if (flags & WS_RUN_POSGRAD) count += launch_posgrad(ctx, c0, nc, s);
     ctx.launches_last_run = count;
 }
 

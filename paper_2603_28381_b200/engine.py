@@ -115,7 +115,7 @@ class DeviceDesign:
     def set_values(self, corner: int, stream=None, **arrays):
         """Replace value arrays of one corner (numpy host arrays or torch CUDA
         tensors): mem_res, mem_cap, root_cap, lut_t_flat, pi_arrival, pi_slew,
-        ep_required."""
+        ep_required; position model: xy, res0, cap0, wire (see placement.py)."""
         L = lib()
         for name, a in arrays.items():
             f = _lib.VALUE_FIELDS[name]
@@ -177,7 +177,17 @@ class DeviceDesign:
             return (self.n_members, 2)
         if name == "summary":
             return (3,)
-        if name in ("mem_res", "mem_cap"):
+        if name in ("d_res", "d_cap"):
+            return (self.n_members, 2)
+        if name == "d_root_cap":
+            return (self.n_nets, 2)
+        if name in ("d_slew", "d_xy", "xy"):
+            return (self.n_pins, 2)
+        if name == "d_len":
+            return (self.n_members,)
+        if name == "wire":
+            return (8,)
+        if name in ("mem_res", "mem_cap", "res0", "cap0"):
             return (self.n_members, 4)
         if name == "root_cap":
             return (self.n_nets, 4)

@@ -1,0 +1,139 @@
+"""GPU parity of the position model and position gradients (ws_place.cu,
+WS_RUN_WIRE | WS_RUN_POSGRAD) against the CPU oracle, which
+test_place_oracle.py pins by finite differences.
+
+Through the C ABI: the wire RC (mem_res / mem_cap written by k_wire) and the
+hard pass on it are bit-exact; d_slew, d_root_cap, d_res, d_cap, d_len and
+d_xy follow the oracle's operation order and are held to 1e-12 relative
+(north_star's gradient bar is 1e-4; the LSE exp/log ulps are the only
+source of difference).
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import ST_FIELDS, grad_close, load, raw_of
+import paper_2603_28381_b200 as ws
+from paper_2603_28381_b200 import _lib, generator as G, placement as PL
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+PG_FIELDS = (("d_slew", "d_slew"), ("d_root_cap", "d_root_cap"), ("d_res", "d_res"),
+             ("d_cap", "d_cap"), ("d_len", "g_len"), ("d_xy", "d_xy"))
+
+
+def oracle_place(raw, pl, loss="hinge"):
+    flat = O.flatten_raw(raw)
+    res, cap = O.wire(flat, pl.xy, pl.res0, pl.cap0, pl.wire.r_unit, pl.wire.c_unit)
+    f = O.with_values(flat, mem_res=res, mem_cap=cap)
+    st = O.run_engine(f)
+    gr = O.timing_gradients(f, st, gamma=0.01 * flat.clock_period, loss=loss)
+    pg = O.position_gradients(f, st, gr, pl.xy, pl.wire.r_unit, pl.wire.c_unit)
+    return flat, res, cap, st, gr, pg
+
+
+def check(dev, corner, raw, pl, loss="hinge", rtol=1e-12):
+    flat, res, cap, st, gr, pg = oracle_place(raw, pl, loss)
+    t_res = dev.value_tensor("mem_res", corner).cpu().numpy()
+    t_cap = dev.value_tensor("mem_cap", corner).cpu().numpy()
+    assert np.array_equal(t_res, res) and np.array_equal(t_cap, cap)
+    for f in ST_FIELDS:
+        assert np.array_equal(dev.get(f, corner), getattr(st, f)), f
+    tns, wns, lossv = dev.summary(corner)
+    assert tns == O.tns(st, flat) and wns == O.wns(st, flat)
+    assert abs(lossv - gr.loss) <= 1e-9 * abs(gr.loss)
+    for name, oname in PG_FIELDS:
+        a, b = dev.get(name, corner), getattr(pg, oname)
+        assert grad_close(a, b, rtol=rtol), (name, np.abs(a - b).max(), np.abs(b).max())
+    return pg
+
+
+def gen(n, topo="star", seed=3):
+    return G.generate_raw(G.GeneratorConfig(num_cells=n, fanout=G.power_law(2.0, 16),
+                                            depth_target=8, seed=seed, net_topology=topo))
+
+
+@pytest.mark.parametrize("topo", ["star", "random_tree"])
+@pytest.mark.parametrize("loss", ["hinge", "softplus"])
+def test_place_step_matches_oracle(topo, loss):
+    raw = gen(600, topo)
+    pl = PL.synthetic_placement(raw, seed=2)
+    dev = ws.DeviceDesign(raw)
+    timer = PL.PlacementTimer(dev, pl, loss=loss)
+    timer.step()
+    check(dev, 0, raw, pl, loss)
+    dev.close()
+
+
+def test_place_edge_kinds():
+    raw = raw_of(load("edge_kinds"))
+    pl = PL.synthetic_placement(raw, seed=5)
+    dev = ws.DeviceDesign(raw)
+    PL.PlacementTimer(dev, pl, loss="softplus").step()
+    check(dev, 0, raw, pl, "softplus")
+    dev.close()
+
+
+def test_place_c1_graph_replay_new_positions():
+    """Graph-captured steps with changing positions equal fresh oracle runs."""
+    raw = G.generate_raw(G.config_c1())
+    pl = PL.synthetic_placement(raw, seed=7)
+    dev = ws.DeviceDesign(raw)
+    timer = PL.PlacementTimer(dev, pl, graph=True)
+    rng = np.random.default_rng(11)
+    for it in range(3):
+        xy = pl.xy + rng.normal(0.0, 2.0, pl.xy.shape) * (it > 0)
+        timer.step(xy)
+        pl2 = PL.Placement(xy=xy, res0=pl.res0, cap0=pl.cap0, wire=pl.wire,
+                           cell_of_pin=pl.cell_of_pin, cell_xy=pl.cell_xy, pin_offset=pl.pin_offset)
+        check(dev, 0, raw, pl2)
+    dev.close()
+
+
+def test_place_corners_independent():
+    raw = gen(400, "random_tree", seed=9)
+    pa = PL.synthetic_placement(raw, seed=1)
+    pb = PL.synthetic_placement(raw, seed=2)
+    dev = ws.DeviceDesign(raw, n_corners=2)
+    ta = PL.PlacementTimer(dev, pa, corner=0)
+    tb = PL.PlacementTimer(dev, pb, corner=1)
+    dev.run(PL.PlacementTimer.FLAGS, corner=0, n_corners=2)
+    check(dev, 0, raw, pa)
+    check(dev, 1, raw, pb)
+    assert ta.corner == 0 and tb.corner == 1
+    dev.close()
+
+
+def test_place_identity_without_positions():
+    """With the default model (xy = 0, wire = 0, base RC = the design's RC)
+    RUN_WIRE reproduces the design's values: the pass equals run_engine."""
+    raw = gen(300)
+    dev = ws.DeviceDesign(raw)
+    dev.run(_lib.RUN_WIRE | _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED
+            | _lib.RUN_POSGRAD)
+    st = O.run_engine(O.flatten_raw(raw))
+    for f in ST_FIELDS:
+        assert np.array_equal(dev.get(f), getattr(st, f)), f
+    assert np.all(dev.get("d_xy") == 0.0)     # all positions equal: sign(0) = 0
+    dev.close()
+
+
+def test_posgrad_needs_grad_pass():
+    raw = gen(100)
+    dev = ws.DeviceDesign(raw)
+    with pytest.raises(RuntimeError):
+        dev.run(_lib.RUN_HARD | _lib.RUN_POSGRAD)
+    dev.close()
+
+
+def test_place_c3_full_size():
+    """C3 (2.49M pins) placement step: hard pass bit-exact on the wire RC,
+    position gradients vs the oracle."""
+    raw = G.generate_raw(G.config_c3())
+    pl = PL.synthetic_placement(raw, seed=3)
+    dev = ws.DeviceDesign(raw)
+    PL.PlacementTimer(dev, pl).step()
+    pg = check(dev, 0, raw, pl)
+    assert np.count_nonzero(pg.d_xy) > 0
+    dev.close()
