@@ -83,6 +83,9 @@ struct PlaceTopo {
     int* parent_pin = nullptr;   // [M] parent pin of each member edge
     int* pc_ptr = nullptr;       // [P+1] member edges whose parent is the pin
     int* pc_mem = nullptr;       // [M]   (ascending member index)
+    int* tm_f = nullptr;         // [M] task-order member slot -> original member index
+    int* tm_root = nullptr;      // [M] task-order member slot -> root pin of its net
+    std::vector<int> tq_mptr_host;   // [N+1] first task-order member slot of level position q
     bool ready = false;
 };
 
@@ -99,6 +102,7 @@ struct PlaceCorner {
     double* g_len = nullptr;     // (M)   dL/dlength
     double* d_xy = nullptr;      // (P,2)
     double *sc_gimp = nullptr, *sc_buf = nullptr, *sc_acc = nullptr;   // (M,2) scratch
+    double* sc_t = nullptr;      // (M,2) root-slew terms of the members
 };
 
 struct CornerSlot {

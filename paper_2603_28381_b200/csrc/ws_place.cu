@@ -29,14 +29,14 @@ namespace {
 
 constexpr double INF = __builtin_huge_val();
 
-struct Lut {
-    const int *s_ptr, *l_ptr, *t_ptr;
-    const double *s, *l, *t;
-};
+__device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
+{
+    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
 
 // d out / d qs and d out / d ql of _interp (_kernels.pyx:15-81) inside the
 // located cell; 0 along an axis whose fraction was clamped (orc interp_grad)
-__device__ void interp_grad(const Lut& L, int lut, double qs, double ql, double& ds, double& dl)
+__device__ __forceinline__ void interp_grad(const LutView& L, int lut, double qs, double ql, double& ds, double& dl)
 {
     const int s0 = L.s_ptr[lut], nS = L.s_ptr[lut + 1] - s0;
     const int l0 = L.l_ptr[lut], nL = L.l_ptr[lut + 1] - l0;
@@ -97,71 +97,24 @@ __global__ void k_wire(int M, const int* __restrict__ mem_pin, const int* __rest
                           __dadd_rn(c0.z, __dmul_rn(wire[6], l)), __dadd_rn(c0.w, __dmul_rn(wire[7], l)));
 }
 
-// one reverse level: thread = (net of the level, late column j)
-__global__ void __launch_bounds__(128) k_pg_level(Topo t, Lut L, Corner C, PlaceCorner G, int q0, int nq)
+// one reverse level.  An 8-lane group per net (4 nets per warp): lane =
+// 8 * group + 2 * slot + j (j = late column), 4 members / in-arcs per round.
+// Member phase (slew adjoint of each member from its out-arcs and the
+// feedthrough net it roots; on star nets the Elmore adjoint up to the
+// dL/dload term) -> ordered group sum of the root-slew terms -> root (winner,
+// LUT partials of the in-arcs, dL/dload, in arc order) -> d_cap.  RC-tree
+// nets run the oracle's sequential recursion (pg_tree_net).  Every load of
+// round 0 is issued before the first store so a net costs ~3 dependent
+// memory hops.
+constexpr int PG_WARPS = 8, PG_G = 8, PG_S = PG_G / 2;
+
+__device__ void pg_tree_net(const Topo& t, const Corner& C, const PlaceCorner& G, int s, int m,
+                            int j, double gl)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 2 * nq) return;
-    const int net = t.lv_nets[q0 + (i >> 1)], j = i & 1, c = 2 + j;
-    const int s = t.net_ptr[net], e = t.net_ptr[net + 1], m = e - s, root = t.net_root[net];
-    double* gimp = G.sc_gimp + (size_t)s * 2 + j;     // member scratch, stride 2
+    const int c = 2 + j;
+    double* gimp = G.sc_gimp + (size_t)s * 2 + j;
     double* buf = G.sc_buf + (size_t)s * 2 + j;
     double* acc = G.sc_acc + (size_t)s * 2 + j;
-    const double sr = C.slew[(size_t)root * 4 + c];
-    double gsum = 0.0, gl = 0.0;
-    // members: slew adjoint (out-arcs + the feedthrough net they root)
-    for (int k = 0; k < m; k++) {
-        const int pin = t.mem_pin[s + k];
-        double g = 0.0;
-        for (int q = t.pin_out_ptr[pin]; q < t.pin_out_ptr[pin + 1]; q++)
-            g = __dadd_rn(g, G.gsa[(size_t)t.pin_out_arc[q] * 2 + j]);
-        if (t.root_net_of_pin[pin] >= 0) g = __dadd_rn(g, G.gsr[(size_t)pin * 2 + j]);
-        G.gs[(size_t)pin * 2 + j] = g;
-        const double sm = C.slew[(size_t)pin * 4 + c];
-        if (sm > 0.0) {
-            gsum = __dadd_rn(gsum, __dmul_rn(g, __ddiv_rn(sr, sm)));
-            gimp[2 * k] = __dmul_rn(g, __ddiv_rn(C.impulse[(size_t)pin * 4 + c], sm));
-        } else {
-            gimp[2 * k] = 0.0;
-        }
-    }
-    const int kind = t.root_kind[net];
-    if (kind == ROOT_FEED) {
-        G.gsr[(size_t)root * 2 + j] = gsum;
-    } else {
-        double groot = gsum;
-        for (int q = t.pin_out_ptr[root]; q < t.pin_out_ptr[root + 1]; q++)
-            groot = __dadd_rn(groot, G.gsa[(size_t)t.pin_out_arc[q] * 2 + j]);
-        G.gs[(size_t)root * 2 + j] = groot;
-        if (kind == ROOT_ARC) {
-            const double ld = C.load[(size_t)root * 4 + c];
-            const int a0 = t.net_in_ptr[net], a1 = t.net_in_ptr[net + 1];
-            double best = -INF;
-            int w = -1;
-            for (int q = a0; q < a1; q++) {
-                const int a = t.net_in_arc[q];
-                const double v = __dadd_rn(C.arrival[(size_t)t.arc_from[a] * 4 + c], C.arc_delay[(size_t)a * 4 + c]);
-                if (v > best) { best = v; w = a; }
-            }
-            for (int q = a0; q < a1; q++) {
-                const int a = t.net_in_arc[q];
-                double ds, dl;
-                interp_grad(L, t.arc_dlut[(size_t)a * 4 + c], C.slew[(size_t)t.arc_from[a] * 4 + c], ld, ds, dl);
-                const double da = C.d_arc[(size_t)a * 2 + j];
-                G.gsa[(size_t)a * 2 + j] = __dmul_rn(da, ds);
-                gl = __dadd_rn(gl, __dmul_rn(da, dl));
-            }
-            if (w >= 0) {
-                double ds, dl;
-                interp_grad(L, t.arc_slut[(size_t)w * 4 + c], C.slew[(size_t)t.arc_from[w] * 4 + c], ld, ds, dl);
-                G.gsa[(size_t)w * 2 + j] = __dadd_rn(G.gsa[(size_t)w * 2 + j], __dmul_rn(groot, ds));
-                gl = __dadd_rn(gl, __dmul_rn(groot, dl));
-            }
-        }
-    }
-    G.gl[(size_t)net * 2 + j] = gl;
-    G.d_root_cap[(size_t)net * 2 + j] = gl;
-    // Elmore adjoint of the net (rc_level order, _kernels.pyx:118-151)
     for (int k = 0; k < m; k++) buf[2 * k] = C.mem_cap[(size_t)(s + k) * 4 + c];
     for (int k = m - 1; k > 0; k--) {
         const int pl = t.mem_parent_loc[s + k];
@@ -202,48 +155,233 @@ __global__ void __launch_bounds__(128) k_pg_level(Topo t, Lut L, Corner C, Place
     }
 }
 
-// dL/dlength of member edge k (orc_pos_reduce, first line)
-__global__ void k_pg_len(int M, PlaceCorner G)
+// member phase of one reverse level, thread = (member slot u of the level in
+// task order, late column j): slew adjoint g from the member's out-arcs and
+// the feedthrough net it roots; impulse adjoint; the root-slew term
+// g * (sr / sm); on star nets the Elmore adjoint up to the dL/dload term
+//   A = adj + gimp (r cap - d) / imp,  d_res = A cap + gimp cap d / imp,
+//   x = A r,  y = gimp r d / imp   (d_cap = (x + gl) + y, k_pg_level)
+// (orc_posgrad_level with buf = cap).  RC-tree nets keep gimp only.
+__global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, Corner C, PlaceCorner G,
+                                                int u_begin, int n2)
 {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= M) return;
-    const double* w = G.wire;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n2) return;
+    const int u = u_begin + (i >> 1), j = i & 1, c = 2 + j;
+    const int pin = t.tm_pin[u], o1 = t.tm_o1_arc[u], fl = t.tm_flags[u];
+    const int f = pt.tm_f[u], root = pt.tm_root[u];
+    const bool tree = t.net_tree[t.mem_net[f]] != 0;
+    const double sm = C.slew[(size_t)pin * 4 + c], im = C.impulse[(size_t)pin * 4 + c];
+    const double sr = C.slew[(size_t)root * 4 + c];
+    const double rr = C.mem_res[(size_t)f * 4 + c], cp = C.mem_cap[(size_t)f * 4 + c];
+    const double d = C.net_delay[(size_t)pin * 4 + c], adj = C.adjoint[(size_t)pin * 2 + j];
     double g = 0.0;
-    for (int j = 0; j < 2; j++)
-        g = __dadd_rn(g, __dadd_rn(__dmul_rn(G.d_res[(size_t)k * 2 + j], w[2 + j]),
-                                   __dmul_rn(G.d_cap[(size_t)k * 2 + j], w[6 + j])));
-    G.g_len[k] = g;
+    if (o1 >= 0) {
+        g = __dadd_rn(g, G.gsa[(size_t)o1 * 2 + j]);
+        for (int v = t.tm_optr[u] + 1; v < t.tm_optr[u + 1]; v++)
+            g = __dadd_rn(g, G.gsa[(size_t)t.to_arc[v] * 2 + j]);
+    }
+    if (fl & TM_ROOT) g = __dadd_rn(g, G.gsr[(size_t)pin * 2 + j]);
+    G.gs[(size_t)pin * 2 + j] = g;
+    double gi = 0.0, tk = 0.0;
+    if (sm > 0.0) {
+        tk = __dmul_rn(g, __ddiv_rn(sr, sm));
+        gi = __dmul_rn(g, __ddiv_rn(im, sm));
+    }
+    const size_t fj = (size_t)f * 2 + j;
+    G.sc_t[fj] = tk;
+    if (tree) {
+        G.sc_gimp[fj] = gi;
+        return;
+    }
+    double a = adj;
+    if (im > 0.0) a = __dadd_rn(a, __dmul_rn(gi, __ddiv_rn(__dsub_rn(__dmul_rn(rr, cp), d), im)));
+    double dr = __dmul_rn(a, cp);
+    if (im > 0.0) dr = __dadd_rn(dr, __dmul_rn(gi, __ddiv_rn(__dmul_rn(cp, d), im)));
+    G.d_res[fj] = dr;
+    G.sc_buf[fj] = __dmul_rn(a, rr);
+    G.sc_acc[fj] = im > 0.0 ? __dmul_rn(gi, __ddiv_rn(__dmul_rn(rr, d), im)) : 0.0;
+}
+
+__global__ void __launch_bounds__(PG_WARPS * 32, 3) k_pg_level(Topo t, LutSrc ls, bool use_smem,
+                                                               Corner C, PlaceCorner G, int q0, int nq)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem);
+    const int lane = threadIdx.x & 31, grp = lane / PG_G, j = lane & 1, c = 2 + j;
+    const int slot = (lane % PG_G) >> 1;
+    const int wq = (blockIdx.x * PG_WARPS + (threadIdx.x >> 5)) * (32 / PG_G);
+    if (wq >= nq) return;                        // whole warp idle
+    const int qi = wq + grp;
+    const bool act = qi < nq;
+    // ---- hop 1: level-major task records of the group's net
+    int net = 0, root = 0, fl = ROOT_PI, f0 = 0, u0 = 0, m = 0, a0 = 0, na = 0;
+    if (act) {
+        const int q = q0 + qi;
+        net = t.lv_nets[q]; root = t.tq_root[q]; fl = t.tq_flags[q]; f0 = t.tq_f0[q];
+        u0 = t.tq_mptr[q]; m = t.tq_mptr[q + 1] - u0;
+        a0 = t.tq_aptr[q]; na = t.tq_aptr[q + 1] - a0;
+    }
+    const int kind = fl & TQ_KIND;
+    const bool tree = fl & TQ_TREE;
+    int rm = (m + PG_S - 1) / PG_S, ra = (na + PG_S - 1) / PG_S;
+    for (int o = 16; o > 0; o >>= 1) {
+        rm = max(rm, __shfl_xor_sync(WS_FULL, rm, o));
+        ra = max(ra, __shfl_xor_sync(WS_FULL, ra, o));
+    }
+    // ---- hop 2 / 3 of round 0: root, first in-arc slot, first member slot
+    const double sr = act ? C.slew[(size_t)root * 4 + c] : 0.0;
+    const double ld = (act && kind == ROOT_ARC) ? C.load[(size_t)root * 4 + c] : 0.0;
+    struct Arc { double v, sf, da; int a; unsigned short dl, sl; };
+    auto load_arc = [&](int qa) {
+        Arc r{-INF, 0.0, 0.0, -1, 0, 0};
+        if (kind == ROOT_ARC && qa < na) {
+            const int fp = t.ta_from[a0 + qa];
+            r.a = t.ta_arc[a0 + qa];
+            r.dl = lut_c(t.ta_lut[2 * (size_t)(a0 + qa)], c);
+            r.sl = lut_c(t.ta_lut[2 * (size_t)(a0 + qa) + 1], c);
+            r.v = __dadd_rn(C.arrival[(size_t)fp * 4 + c], C.arc_delay[(size_t)r.a * 4 + c]);
+            r.sf = C.slew[(size_t)fp * 4 + c];
+            r.da = C.d_arc[(size_t)r.a * 2 + j];
+        }
+        return r;
+    };
+    const Arc arc0 = load_arc(slot);
+    // ---- root-slew terms of the members (k_pg_mem), summed in slot order
+    const double* __restrict__ sct = G.sc_t;
+    double part = 0.0;
+#pragma unroll 4
+    for (int r = 0; r < rm; r++) {
+        const int k = r * PG_S + slot;
+        if (k < m) part = __dadd_rn(part, sct[(size_t)(f0 + k) * 2 + j]);
+    }
+    // fixed-order sum over the slots of column j within the group
+    for (int o = 2; o < PG_G; o <<= 1) part = __dadd_rn(part, __shfl_xor_sync(WS_FULL, part, o, PG_G));
+    const double gsum = part;
+    // ---- root
+    double gl = 0.0, groot = gsum;
+    if (act && kind == ROOT_FEED && slot == 0) G.gsr[(size_t)root * 2 + j] = gsum;
+    if (act && kind != ROOT_FEED && slot == 0) {
+        for (int v = t.pin_out_ptr[root]; v < t.pin_out_ptr[root + 1]; v++)
+            groot = __dadd_rn(groot, G.gsa[(size_t)t.pin_out_arc[v] * 2 + j]);
+        G.gs[(size_t)root * 2 + j] = groot;
+    }
+    groot = __shfl_sync(WS_FULL, groot, j, PG_G);
+    // winner: late = first strict max over the in-arcs in order
+    double best = -INF;
+    int w = -1;
+    for (int r = 0; r < ra; r++) {
+        const Arc A = r == 0 ? arc0 : load_arc(r * PG_S + slot);
+        for (int k = 0; k < PG_S; k++) {
+            const double vk = __shfl_sync(WS_FULL, A.v, 2 * k + j, PG_G);
+            if (r * PG_S + k < na && vk > best) { best = vk; w = r * PG_S + k; }
+        }
+    }
+    double slw = 0.0;
+    for (int r = 0; r < ra; r++) {
+        const int qa = r * PG_S + slot;
+        const Arc A = r == 0 ? arc0 : load_arc(qa);
+        double term = 0.0, sl = 0.0;
+        if (qa < na && kind == ROOT_ARC) {
+            double ds, dl;
+            interp_grad(L, A.dl, A.sf, ld, ds, dl);
+            double ga = __dmul_rn(A.da, ds);
+            term = __dmul_rn(A.da, dl);
+            if (qa == w) {
+                double ss;
+                interp_grad(L, A.sl, A.sf, ld, ss, sl);
+                ga = __dadd_rn(ga, __dmul_rn(groot, ss));
+            }
+            G.gsa[(size_t)A.a * 2 + j] = ga;
+        }
+        for (int k = 0; k < PG_S; k++) {          // arc order (oracle order)
+            const double tk = __shfl_sync(WS_FULL, term, 2 * k + j, PG_G);
+            if (r * PG_S + k < na) gl = __dadd_rn(gl, tk);
+        }
+        const bool here = w >= r * PG_S && w < (r + 1) * PG_S;
+        const double slr = __shfl_sync(WS_FULL, sl, here ? 2 * (w - r * PG_S) + j : j, PG_G);
+        if (here) slw = slr;
+    }
+    if (w >= 0) gl = __dadd_rn(gl, __dmul_rn(groot, slw));
+    if (!act) return;
+    if (slot == 0) {
+        G.gl[(size_t)net * 2 + j] = gl;
+        G.d_root_cap[(size_t)net * 2 + j] = gl;
+    }
+    // ---- Elmore adjoint: finish d_cap (star) / the oracle's recursion (tree)
+    if (tree) {
+        if (slot == 0) pg_tree_net(t, C, G, f0, m, j, gl);
+        return;
+    }
+    const double* __restrict__ xs = G.sc_buf;
+    const double* __restrict__ ys = G.sc_acc;
+    double* __restrict__ dcap = G.d_cap;
+#pragma unroll 4
+    for (int k = slot; k < m; k += PG_S) {
+        const size_t f = (size_t)(f0 + k) * 2 + j;
+        dcap[f] = __dadd_rn(__dadd_rn(xs[f], gl), ys[f]);
+    }
 }
 
 __device__ __forceinline__ double sgn(double d) { return d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0); }
 
-// dL/dxy of pin p: its own edge (as a member) and the edges of its children
+// dL/dlength of member edge k and its signed x / y contributions
+// e_k = dL/dlength * sign(member - parent) (orc_pos_reduce's g * sg)
+__global__ void k_pg_len(int M, const int* __restrict__ mem_pin, const int* __restrict__ parent_pin,
+                         PlaceCorner G)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= M) return;
+    const double* w = G.wire;
+    const double2 dr = reinterpret_cast<const double2*>(G.d_res)[k];
+    const double2 dc = reinterpret_cast<const double2*>(G.d_cap)[k];
+    double g = 0.0;
+    g = __dadd_rn(g, __dadd_rn(__dmul_rn(dr.x, w[2]), __dmul_rn(dc.x, w[6])));
+    g = __dadd_rn(g, __dadd_rn(__dmul_rn(dr.y, w[3]), __dmul_rn(dc.y, w[7])));
+    G.g_len[k] = g;
+    const double2 xp = reinterpret_cast<const double2*>(G.xy)[mem_pin[k]];
+    const double2 xq = reinterpret_cast<const double2*>(G.xy)[parent_pin[k]];
+    reinterpret_cast<double2*>(G.sc_buf)[k] =
+        make_double2(__dmul_rn(g, sgn(__dsub_rn(xp.x, xq.x))), __dmul_rn(g, sgn(__dsub_rn(xp.y, xq.y))));
+}
+
+// dL/dxy of pin p: + its own edge (as a member), - the edges of its children
 // (as a parent), merged in ascending member order = orc_pos_reduce's order
-__global__ void k_pg_xy(int P, Topo t, PlaceTopo pt, PlaceCorner G)
+__global__ void k_pg_xy(int P, const int* __restrict__ member_of_pin, const int* __restrict__ pc_ptr,
+                        const int* __restrict__ pc_mem, const double2* __restrict__ e,
+                        double2* __restrict__ d_xy)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
-    const double2 xp = reinterpret_cast<const double2*>(G.xy)[p];
-    const int own = t.member_of_pin[p];
+    const int own = member_of_pin[p];
+    const int q0 = pc_ptr[p], q1 = pc_ptr[p + 1];
     double gx = 0.0, gy = 0.0;
     bool own_done = own < 0;
-    auto add_own = [&]() {
-        const double2 xq = reinterpret_cast<const double2*>(G.xy)[pt.parent_pin[own]];
-        const double g = G.g_len[own];
-        gx = __dadd_rn(gx, __dmul_rn(g, sgn(__dsub_rn(xp.x, xq.x))));
-        gy = __dadd_rn(gy, __dmul_rn(g, sgn(__dsub_rn(xp.y, xq.y))));
+    if (!own_done && (q0 == q1 || own < pc_mem[q0])) {
+        const double2 v = e[own];
+        gx = __dadd_rn(gx, v.x);
+        gy = __dadd_rn(gy, v.y);
         own_done = true;
-    };
-    for (int q = pt.pc_ptr[p]; q < pt.pc_ptr[p + 1]; q++) {
-        const int k = pt.pc_mem[q];
-        if (!own_done && own < k) add_own();
-        const double2 xk = reinterpret_cast<const double2*>(G.xy)[t.mem_pin[k]];
-        const double g = G.g_len[k];
-        gx = __dsub_rn(gx, __dmul_rn(g, sgn(__dsub_rn(xk.x, xp.x))));
-        gy = __dsub_rn(gy, __dmul_rn(g, sgn(__dsub_rn(xk.y, xp.y))));
     }
-    if (!own_done) add_own();
-    reinterpret_cast<double2*>(G.d_xy)[p] = make_double2(gx, gy);
+#pragma unroll 4
+    for (int q = q0; q < q1; q++) {
+        const int k = pc_mem[q];
+        if (!own_done && own < k) {
+            const double2 v = e[own];
+            gx = __dadd_rn(gx, v.x);
+            gy = __dadd_rn(gy, v.y);
+            own_done = true;
+        }
+        const double2 v = e[k];
+        gx = __dsub_rn(gx, v.x);
+        gy = __dsub_rn(gy, v.y);
+    }
+    if (!own_done) {
+        const double2 v = e[own];
+        gx = __dadd_rn(gx, v.x);
+        gy = __dadd_rn(gy, v.y);
+    }
+    d_xy[p] = make_double2(gx, gy);
 }
 
 }  // namespace
@@ -274,7 +412,26 @@ void place_enable(Context& ctx)
         std::vector<int> fill(cptr.begin(), cptr.end() - 1);
         for (int k = 0; k < M; k++) cmem[fill[par[k]]++] = k;   // ascending k per pin
     }
+    // task-order member slot -> original member index / root pin
+    std::vector<int> tq_mptr(N + 1), tq_f0(N), tq_root(N), tm_f(M), tm_root(M);
+    WS_CUDA(cudaMemcpy(tq_mptr.data(), t.tq_mptr, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
+    if (N) {
+        WS_CUDA(cudaMemcpy(tq_f0.data(), t.tq_f0, sizeof(int) * N, cudaMemcpyDeviceToHost));
+        WS_CUDA(cudaMemcpy(tq_root.data(), t.tq_root, sizeof(int) * N, cudaMemcpyDeviceToHost));
+    }
+    for (int q = 0; q < N; q++)
+        for (int u = tq_mptr[q]; u < tq_mptr[q + 1]; u++) {
+            tm_f[u] = tq_f0[q] + (u - tq_mptr[q]);
+            tm_root[u] = tq_root[q];
+        }
+    ctx.pt.tq_mptr_host = tq_mptr;
     Arena& ar = ctx.topo_mem;
+    ctx.pt.tm_f = ar.alloc<int>(std::max(M, 1));
+    ctx.pt.tm_root = ar.alloc<int>(std::max(M, 1));
+    if (M) {
+        WS_CUDA(cudaMemcpy(ctx.pt.tm_f, tm_f.data(), sizeof(int) * M, cudaMemcpyHostToDevice));
+        WS_CUDA(cudaMemcpy(ctx.pt.tm_root, tm_root.data(), sizeof(int) * M, cudaMemcpyHostToDevice));
+    }
     ctx.pt.parent_pin = ar.alloc<int>(std::max(M, 1));
     ctx.pt.pc_ptr = ar.alloc<int>(P + 1);
     ctx.pt.pc_mem = ar.alloc<int>(std::max(M, 1));
@@ -306,6 +463,7 @@ void place_enable(Context& ctx)
         g.sc_gimp = vr.alloc<double>(2 * (size_t)M);
         g.sc_buf = vr.alloc<double>(2 * (size_t)M);
         g.sc_acc = vr.alloc<double>(2 * (size_t)M);
+        g.sc_t = vr.alloc<double>(2 * (size_t)M);
         WS_CUDA(cudaMemset(g.xy, 0, sizeof(double) * 2 * std::max(P, 1)));
         WS_CUDA(cudaMemset(g.wire, 0, sizeof(double) * 8));
         if (M) {
@@ -314,7 +472,7 @@ void place_enable(Context& ctx)
         }
         for (double* z : {g.gs, g.gsr, g.d_xy})
             WS_CUDA(cudaMemset(z, 0, sizeof(double) * 2 * std::max(P, 1)));
-        for (double* z : {g.d_res, g.d_cap, g.sc_gimp, g.sc_buf, g.sc_acc})
+        for (double* z : {g.d_res, g.d_cap, g.sc_gimp, g.sc_buf, g.sc_acc, g.sc_t})
             WS_CUDA(cudaMemset(z, 0, sizeof(double) * 2 * std::max(M, 1)));
         WS_CUDA(cudaMemset(g.g_len, 0, sizeof(double) * std::max(M, 1)));
         WS_CUDA(cudaMemset(g.gsa, 0, sizeof(double) * 2 * std::max(t.A, 1)));
@@ -344,25 +502,38 @@ int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s)
 {
     const Topo& t = ctx.t;
     int count = 0;
+    const LutSrc ls{t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, t.NL,
+                    ctx.lut_s_len, ctx.lut_l_len, ctx.lut_t_len, t.lut_info};
+    // the 9 KB pool stays L1-resident; per-block smem staging would cost more
+    // than the few located queries of a net's in-arcs
+    const size_t lut_bytes = 0;
+    const bool use_smem = false;
     for (int k = c0; k < c0 + nc; k++) {
         const PlaceCorner& g = ctx.place[k];
         const Corner& d = ctx.corners[k].d;
-        const Lut L{t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, d.lut_t_flat};
         // arcs of lower-level targets are read before written: start from 0
         if (t.A) WS_CUDA(cudaMemsetAsync(g.gsa, 0, sizeof(double) * 2 * (size_t)t.A, s));
         if (t.P) WS_CUDA(cudaMemsetAsync(g.gsr, 0, sizeof(double) * 2 * (size_t)t.P, s));
         for (int li = t.L - 1; li >= 0; li--) {
             const int q0 = ctx.lv_ptr_host[li], nq = ctx.lv_ptr_host[li + 1] - q0;
             if (nq <= 0) continue;
-            k_pg_level<<<(2 * nq + 127) / 128, 128, 0, s>>>(t, L, d, g, q0, nq);
+            const int ub = ctx.pt.tq_mptr_host[q0], un = ctx.pt.tq_mptr_host[q0 + nq] - ub;
+            if (un > 0) {
+                k_pg_mem<<<(2 * un + 255) / 256, 256, 0, s>>>(t, ctx.pt, d, g, ub, 2 * un);
+                count++;
+            }
+            k_pg_level<<<(nq + PG_WARPS * (32 / PG_G) - 1) / (PG_WARPS * (32 / PG_G)), PG_WARPS * 32, lut_bytes, s>>>(
+                t, ls, use_smem, d, g, q0, nq);
             count++;
         }
         if (t.M) {
-            k_pg_len<<<(t.M + 255) / 256, 256, 0, s>>>(t.M, g);
+            k_pg_len<<<(t.M + 255) / 256, 256, 0, s>>>(t.M, t.mem_pin, ctx.pt.parent_pin, g);
             count++;
         }
         if (t.P) {
-            k_pg_xy<<<(t.P + 255) / 256, 256, 0, s>>>(t.P, t, ctx.pt, g);
+            k_pg_xy<<<(t.P + 255) / 256, 256, 0, s>>>(
+                t.P, t.member_of_pin, ctx.pt.pc_ptr, ctx.pt.pc_mem,
+                reinterpret_cast<const double2*>(g.sc_buf), reinterpret_cast<double2*>(g.d_xy));
             count++;
         }
         WS_CHECK_LAUNCH();
