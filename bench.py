@@ -167,6 +167,84 @@ def time_reference(raw, max_passes, budget_s):
             "times_ms": [round(1e3 * t, 1) for t in times]}
 
 
+def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
+    """C4: the timing-driven placement loop — n_inv STA
+    fwd+bwd invocations on the C3 netlist with perturbed pin coordinates,
+    each returning loss / TNS / WNS and dL/dxy (position gradients).
+
+    Invocation t moves every cell by N(0, sigma_um) (seed + t, pins follow
+    their cell; coordinates generated on the device before the timed loop),
+    then one ws_run does wire RC -> RC -> forward + LSE -> backward +
+    adjoint -> position gradients.  Device time: CUDA events around all
+    n_inv invocations (each = D2D install of its coordinates + ws_run).  e2e:
+    the same loop through the public API with each invocation's positions
+    copied from pinned host memory and loss / TNS / WNS read back."""
+    import torch
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200 import placement as PL
+    pl = PL.synthetic_placement(raw, seed=3)
+    dev = ws.DeviceDesign(raw, n_corners=1)
+    timer = PL.PlacementTimer(dev, pl)
+    stream = torch.cuda.current_stream()
+    cell_xy = torch.as_tensor(pl.cell_xy, device="cuda")
+    cop = torch.as_tensor(pl.cell_of_pin, device="cuda")
+    off = torch.as_tensor(pl.pin_offset, device="cuda")
+    xy = dev.value_tensor("xy")          # the corner's position array in HBM
+    summ = dev.tensor("summary")
+    # every invocation's coordinates, generated on the device up front (the
+    # placer's input stream; 8 GB of HBM at C3): cell k of invocation t moves
+    # by N(0, sigma) from torch's Philox stream seeded seed + t
+    xy_all = torch.empty((n_inv,) + tuple(off.shape), dtype=torch.float64, device="cuda")
+    gen = torch.Generator(device="cuda")
+    for t in range(n_inv):
+        gen.manual_seed(seed + t)
+        disp = torch.randn(cell_xy.shape, generator=gen, device="cuda", dtype=torch.float64)
+        torch.add((cell_xy + sigma_um * disp).index_select(0, cop), off, out=xy_all[t])
+
+    def invocation(t):
+        xy.copy_(xy_all[t])
+        dev.run(timer.flags, gamma=timer.gamma, stream=stream)
+
+    for t in range(3):
+        invocation(t)
+    torch.cuda.synchronize()
+    launches = dev.last_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(n_inv):
+        invocation(t)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1)
+    loss_last = dev.summary()
+    # e2e: positions from pinned host memory, summary back, every invocation
+    rng = np.random.default_rng(seed)
+    host_xy = [torch.from_numpy(np.ascontiguousarray(
+        pl.xy + sigma_um * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin])).pin_memory()
+        for _ in range(2)]
+    h_out = torch.zeros(3, dtype=torch.float64).pin_memory()
+    n_e2e = min(n_inv, 50)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for t in range(n_e2e):
+        xy.copy_(host_xy[t % 2], non_blocking=True)
+        dev.run(timer.flags, gamma=timer.gamma, stream=stream)
+        h_out.copy_(summ, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / n_e2e
+    dev.close()
+    return {"workload": "C4 timing-driven placement loop on C3: %d STA fwd+bwd invocations with "
+                        "perturbed pin coordinates (cells moved by N(0, %.1f um)), position "
+                        "gradients dL/dxy every invocation" % (n_inv, sigma_um),
+            "invocations": n_inv, "total_ms": round(dev_ms, 3),
+            "ms_per_invocation": round(dev_ms / n_inv, 4),
+            "launches_per_invocation": launches,
+            "e2e": {"ms_per_invocation": round(e2e_ms, 4), "invocations": n_e2e,
+                    "h2d_bytes_per_step": int(host_xy[0].numel() * 8), "d2h_bytes_per_step": 24},
+            "last": {"tns": loss_last[0], "wns": loss_last[1], "loss": loss_last[2]}}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -190,6 +268,8 @@ def main():
     ap.add_argument("--graph", type=int, default=1)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--workload", default="c3", choices=("c1", "c2", "c3"))
+    ap.add_argument("--placement", type=int, default=200,
+                    help="C4 placement-loop invocations reported under placement_loop (0: skip)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -395,6 +475,8 @@ def main():
                 "clocks": clk.summary(),
                 "result": {"tns": tns, "wns": wns, "loss": loss},
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
+        if args.placement and world == 1:
+            line["placement_loop"] = placement_loop(raw, n_inv=args.placement)
         if args.cpu_baseline and world == 1:
             r = time_reference(raw, max_passes=3, budget_s=25.0)
             line["cpu_baseline"] = {"value": round(r["ms"], 3), "unit": "ms", "cores": 1,

@@ -4,9 +4,12 @@ test_place_oracle.py pins by finite differences.
 
 Through the C ABI: the wire RC (mem_res / mem_cap written by k_wire) and the
 hard pass on it are bit-exact; d_slew, d_root_cap, d_res, d_cap, d_len and
-d_xy follow the oracle's operation order and are held to 1e-12 relative
-(north_star's gradient bar is 1e-4; the LSE exp/log ulps are the only
-source of difference).
+d_xy follow the oracle's operation order except for the member sums of the
+root-slew terms (a fixed warp-shuffle order); with the LSE exp/log ulps that
+is the only source of difference.  They are held to 1e-9 relative (with a
+1e-9 x max floor), five orders tighter than north_star's 1e-4 bar; d_xy
+sums signed edge terms, so ulp-level input differences can grow by the
+cancellation factor.
 """
 
 import numpy as np
@@ -33,7 +36,7 @@ def oracle_place(raw, pl, loss="hinge"):
     return flat, res, cap, st, gr, pg
 
 
-def check(dev, corner, raw, pl, loss="hinge", rtol=1e-12):
+def check(dev, corner, raw, pl, loss="hinge", rtol=1e-9):
     flat, res, cap, st, gr, pg = oracle_place(raw, pl, loss)
     t_res = dev.value_tensor("mem_res", corner).cpu().numpy()
     t_cap = dev.value_tensor("mem_cap", corner).cpu().numpy()
@@ -45,7 +48,11 @@ def check(dev, corner, raw, pl, loss="hinge", rtol=1e-12):
     assert abs(lossv - gr.loss) <= 1e-9 * abs(gr.loss)
     for name, oname in PG_FIELDS:
         a, b = dev.get(name, corner), getattr(pg, oname)
-        assert grad_close(a, b, rtol=rtol), (name, np.abs(a - b).max(), np.abs(b).max())
+        if not grad_close(a, b, rtol=rtol):
+            d = np.abs(a - b)
+            i = int(np.argmax(d / np.maximum(np.abs(b), 1e-9 * np.abs(b).max())))
+            raise AssertionError(f"{name}: worst rel {d.flat[i] / max(abs(b.flat[i]), 1e-300):.3e} "
+                                 f"at {i} ({a.flat[i]!r} vs {b.flat[i]!r}), max|b| {np.abs(b).max():.3e}")
     return pg
 
 
@@ -136,4 +143,23 @@ def test_place_c3_full_size():
     PL.PlacementTimer(dev, pl).step()
     pg = check(dev, 0, raw, pl)
     assert np.count_nonzero(pg.d_xy) > 0
+    dev.close()
+
+
+def test_place_c4_loop_c3():
+    """C4: 200 graph-replayed placement invocations on C3 with perturbed
+    cell positions (seed 1000 + t); invocations 0, 99 and 199 equal fresh
+    oracle runs on the same coordinates."""
+    raw = G.generate_raw(G.config_c3())
+    pl = PL.synthetic_placement(raw, seed=3)
+    dev = ws.DeviceDesign(raw)
+    timer = PL.PlacementTimer(dev, pl)
+    for t in range(200):
+        rng = np.random.default_rng(1000 + t)
+        xy = pl.xy + 0.5 * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin]
+        timer.step(xy)
+        if t in (0, 99, 199):
+            check(dev, 0, raw, PL.Placement(xy=xy, res0=pl.res0, cap0=pl.cap0, wire=pl.wire,
+                                            cell_of_pin=pl.cell_of_pin, cell_xy=pl.cell_xy,
+                                            pin_offset=pl.pin_offset))
     dev.close()
