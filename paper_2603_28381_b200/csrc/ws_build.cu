@@ -407,6 +407,78 @@ __global__ void k_rc_code(int M, const int* mem_pin, const int* mem_net, const i
 
 
 // Level-major task arrays and the task partition of every level.
+
+// per-task record blobs (see Topo::fb_*): the records of task k's level
+// kernels, laid out by (task, slot) so a block loads them from its task index
+__global__ void k_blob(Topo t)
+{
+    const int k = blockIdx.x, tid = threadIdx.x;
+    const int4 A = t.tk_a[k], B = t.tk_b[k];
+    const int q0 = A.x, nq = A.y, a0 = A.z, na_t = A.w, m0 = B.x, nm = B.y, tflags = B.z;
+    const bool wide = tflags & TK_WIDE;
+    if (tid <= TASK_Q) {
+        int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0);
+        if (tid <= nq) {
+            const int q = q0 + tid;
+            b.y = t.tq_aptr[q];
+            b.z = t.tq_mptr[q];
+            if (tid < nq) {
+                a = make_int4(t.tq_root[q], t.tq_flags[q], t.tq_f0[q], t.lv_nets[q]);
+                b.x = t.tq_e1[q];
+            }
+        }
+        t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + tid)] = a;
+        t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + tid) + 1] = b;
+    }
+    if (tid < TASK_Q) {
+        const int qi = tid;
+        int4 fq = make_int4(-1, 0, 0, 0), bq = make_int4(-1, 0, -1, 0);
+        if (qi < nq) {
+            const int q = q0 + qi;
+            fq.x = t.tq_root[q];
+            fq.y = t.tq_flags[q];
+            if ((fq.y & TQ_KIND) == ROOT_ARC && !wide) {
+                fq.z = t.tq_aptr[q];
+                fq.w = t.tq_aptr[q + 1] - fq.z;
+            }
+            bq = make_int4(fq.x, fq.y, t.tq_e1[q], 0);
+        }
+        t.fb_q[(size_t)k * TASK_Q + qi] = fq;
+        t.bb_q[(size_t)k * TASK_Q + qi] = bq;
+        for (int s = 0; s < 3; s++) {
+            int2 fa = make_int2(0, 0);
+            uint4 fl = make_uint4(0, 0, 0, 0);
+            if (fq.w > 0 && fq.w <= 3) {
+                // slots past the last arc repeat arc 0 (branch-free net phase)
+                const int qa = fq.z + (s < fq.w ? s : 0);
+                fa = make_int2(t.ta_from[qa], t.ta_arc[qa]);
+                const ushort4 d = t.ta_lut[2 * (size_t)qa], l = t.ta_lut[2 * (size_t)qa + 1];
+                fl = make_uint4(d.x | ((unsigned)d.y << 16), d.z | ((unsigned)d.w << 16),
+                                l.x | ((unsigned)l.y << 16), l.z | ((unsigned)l.w << 16));
+            }
+            t.fb_a[((size_t)k * TASK_Q + qi) * 3 + s] = fa;
+            t.fb_l[((size_t)k * TASK_Q + qi) * 3 + s] = fl;
+        }
+    }
+    if (tid < TASK_M) {
+        const int ii = tid;
+        int2 fm = make_int2(-1, 0);
+        int4 m1 = make_int4(-1, 0, -1, -1), m2 = make_int4(-1, 0, 0, -1);
+        if (ii < nm) {
+            const int u = m0 + ii;
+            fm = make_int2(t.tm_pin[u], t.tm_flags[u]);
+            m1 = make_int4(fm.x, fm.y, t.tm_o1_to[u], t.tm_o1_arc[u]);
+            m2.x = t.tm_e1[u];
+            m2.y = t.tm_optr[u];
+            m2.z = t.tm_optr[u + 1] - m2.y;
+        }
+        if (ii < na_t && !wide) m2.w = t.ta_arc[a0 + ii];
+        t.fb_m[(size_t)k * TASK_M + ii] = fm;
+        t.bb_m[2 * ((size_t)k * TASK_M + ii)] = m1;
+        t.bb_m[2 * ((size_t)k * TASK_M + ii) + 1] = m2;
+    }
+}
+
 void build_tasks(Context& ctx)
 {
     Topo& t = ctx.t;
@@ -559,6 +631,20 @@ void build_tasks(Context& ctx)
         k_task_local<<<blocks_for(t.n_tasks), TPB, 0, s>>>(t.n_tasks, t.tk_a, t.tk_b, t.tq_aptr,
                                                            t.tq_mptr, t.ta_q, t.tm_flags);
         WS_CHECK_LAUNCH();
+    }
+    {
+        const size_t T = (size_t)std::max(t.n_tasks, 1);
+        t.fb_n = ar.alloc<int4>(T * (TASK_Q + 1) * 2);
+        t.fb_q = ar.alloc<int4>(T * TASK_Q);
+        t.fb_a = ar.alloc<int2>(T * TASK_Q * 3);
+        t.fb_l = ar.alloc<uint4>(T * TASK_Q * 3);
+        t.fb_m = ar.alloc<int2>(T * TASK_M);
+        t.bb_m = ar.alloc<int4>(T * TASK_M * 2);
+        t.bb_q = ar.alloc<int4>(T * TASK_Q);
+        if (t.n_tasks) {
+            k_blob<<<t.n_tasks, PASS_TPB, 0, s>>>(t);   // after k_task_local: tm_flags final
+            WS_CHECK_LAUNCH();
+        }
     }
     // pins finished after the level loop
     uint8_t* ff = ar.alloc<uint8_t>(P);

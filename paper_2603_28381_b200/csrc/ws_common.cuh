@@ -91,6 +91,16 @@ struct Topo {
     int *bn_part0;     // [n_big] first partial of the slot
     int n_big, n_parts;
     unsigned long long *probe;   // WS_PROBE builds: per-block phase timestamps
+    // per-task record blobs (ws_build.cu: k_blob): every record a level
+    // kernel's prologue needs, at addresses computable from the task index
+    // alone, so the prologue is one dependent memory round trip
+    int4 *fb_n;        // [T * (TASK_Q+1) * 2] NetSmem: {root, flags, f0, net}, {e1, aptr, mptr, 0}
+    int4 *fb_q;        // [T * TASK_Q] forward net item: {root | -1, flags, a0, na (0: not net-centric)}
+    int2 *fb_a;        // [T * TASK_Q * 3] forward in-arc slots: {from, arc}
+    uint4 *fb_l;       // [T * TASK_Q * 3] their delay / slew LUT ids, 2 x 16 bit per word
+    int2 *fb_m;        // [T * TASK_M] member slots: {pin | -1, tm_flags}
+    int4 *bb_m;        // [T * TASK_M * 2] backward member: {pin | -1, fl, o1_to, o1_arc}, {e1, o0, no, arc}
+    int4 *bb_q;        // [T * TASK_Q] backward net item: {root | -1, flags, e1, 0}
     int *fin_pins;     // pins finished after the level loop (free pins, PI roots with out-arcs)
     int *fin_flags;    // 1 = accumulate onto the level-loop adjoint (root), 0 = fresh
     int n_fin;

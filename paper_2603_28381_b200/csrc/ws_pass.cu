@@ -114,6 +114,27 @@ struct NetSmem {
     int mptr[TASK_Q + 1];   // absolute tm_* offsets
 };
 
+// the same records from the task's blob (one round trip, k-indexed)
+__device__ __forceinline__ void load_nets_blob(const Topo& t, int k, const Task& T, NetSmem& S)
+{
+    const int i = threadIdx.x;
+    if (i <= TASK_Q) {
+        const int4 a = t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + i)];
+        const int4 b = t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + i) + 1];
+        if (i <= T.nq) {
+            S.aptr[i] = b.y;
+            S.mptr[i] = b.z;
+            if (i < T.nq) {
+                S.root[i] = a.x;
+                S.flags[i] = a.y;
+                S.f0[i] = a.z;
+                S.net[i] = a.w;
+                S.e1[i] = b.x;
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void load_nets(const Topo& t, const Task& T, NetSmem& S)
 {
     const int i = threadIdx.x;
@@ -482,13 +503,50 @@ __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSme
     }
 }
 
+template <bool HARD>
+__device__ __forceinline__ void fwd_records_blob(const Topo& t, int k, const Task& T, FwdSmem& S, FwdRec& R)
+{
+    load_nets_blob(t, k, T, S.n);
+    const int c = threadIdx.x & 3, qi = threadIdx.x >> 2;
+    const size_t qs = (size_t)k * TASK_Q + qi;
+    // every load below is addressed by (task, slot) only: one round trip
+    const int4 fq = t.fb_q[qs];
+    int2 fa[FWD_NA];
+    uint4 fl[FWD_NA];
+#pragma unroll
+    for (int s = 0; s < FWD_NA; s++) {
+        fa[s] = t.fb_a[qs * FWD_NA + s];
+        if (HARD) fl[s] = t.fb_l[qs * FWD_NA + s];
+    }
+    int2 fm[ITEMS];
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) fm[s] = t.fb_m[(size_t)k * TASK_M + qi + s * TASK_Q];
+    R.nroot = fq.x;
+    R.nflags = fq.y;
+    R.a0 = fq.z;
+    R.na = fq.w;
+#pragma unroll
+    for (int s = 0; s < FWD_NA; s++) {
+        R.from[s] = fa[s].x;
+        R.arc[s] = fa[s].y;
+        if (HARD) {
+            const unsigned dw = c < 2 ? fl[s].x : fl[s].y, sw = c < 2 ? fl[s].z : fl[s].w;
+            R.dl[s] = (unsigned short)((c & 1) ? dw >> 16 : dw & 0xffff);
+            R.sl[s] = (unsigned short)((c & 1) ? sw >> 16 : sw & 0xffff);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) {
+        R.mpin[s] = fm[s].x;
+        R.mfl[s] = fm[s].y;
+    }
+}
+
 // persistent kernel: records plus every gather that is static for the whole
 // forward sweep (RC outputs)
 template <bool HARD>
-__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, const Task& T,
-                                                   FwdSmem& S, FwdRec& R)
+__device__ __forceinline__ void fwd_static_gathers(const Corner& C, FwdRec& R)
 {
-    fwd_records<HARD>(t, T, S, R);
     const int c = threadIdx.x & 3;
 #pragma unroll
     for (int k = 0; k < ITEMS; k++)
@@ -497,6 +555,14 @@ __device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& 
             if (HARD) R.mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
         }
     R.ld = (HARD && R.na > 0) ? LDG(C.load + (size_t)R.nroot * 4 + c) : 0.0;
+}
+
+template <bool HARD>
+__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, int k, const Task& T,
+                                                   FwdSmem& S, FwdRec& R)
+{
+    fwd_records_blob<HARD>(t, k, T, S, R);
+    fwd_static_gathers<HARD>(C, R);
 }
 
 // arc-driven root with more than FWD_NA (but <= TASK_A) in-arcs: the same
@@ -794,6 +860,36 @@ __device__ __forceinline__ void bwd_records(const Topo& t, const Task& T, BwdSme
     }
 }
 
+template <bool GRAD>
+__device__ __forceinline__ void bwd_records_blob(const Topo& t, int k, const Task& T, BwdSmem& S, BwdRec& R)
+{
+    load_nets_blob(t, k, T, S.n);
+    const bool late = (threadIdx.x & 3) >= 2;
+    const int qi = threadIdx.x >> 2;
+    int4 m1[ITEMS], m2[ITEMS];
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) {
+        const size_t ms = (size_t)k * TASK_M + qi + s * TASK_Q;
+        m1[s] = t.bb_m[2 * ms];
+        m2[s] = t.bb_m[2 * ms + 1];
+    }
+    const int4 bq = t.bb_q[(size_t)k * TASK_Q + qi];
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) {
+        R.pin[s] = m1[s].x;
+        R.fl[s] = m1[s].y;
+        R.o1t[s] = m1[s].z;
+        R.o1a[s] = m1[s].w;
+        R.e1[s] = m2[s].x;
+        R.o0[s] = m2[s].y;
+        R.no[s] = m2[s].z;
+        R.arc[s] = (GRAD && late) ? m2[s].w : -1;
+    }
+    R.nroot = bq.x;
+    R.nflags = bq.y;
+    R.ne1 = bq.z;
+}
+
 // one member (u, c): fold required over out-arcs, slack, adjoint.
 template <bool HARD, bool GRAD>
 __device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int o0, int o1, int pin,
@@ -883,10 +979,9 @@ __device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int 
 // persistent kernel: records plus the gathers that are static for the whole
 // backward sweep (forward outputs, endpoint seeds)
 template <bool HARD, bool GRAD>
-__device__ __forceinline__ void bwd_records_static(const Topo& t, const Corner& C, const Task& T,
-                                                   BwdSmem& S, BwdRec& R, double g, int kind)
+__device__ __forceinline__ void bwd_static_gathers(const Topo& t, const Corner& C, BwdRec& R, double g,
+                                                   int kind)
 {
-    bwd_records<GRAD>(t, T, S, R);
     const int c = threadIdx.x & 3, j = c - 2;
     const bool late = c >= 2;
 #pragma unroll
@@ -919,6 +1014,14 @@ __device__ __forceinline__ void bwd_records_static(const Topo& t, const Corner& 
         }
         if (GRAD && late) R.n_seed = root_seed(t, C, R.nroot, R.nflags, R.ne1, j, g, kind);
     }
+}
+
+template <bool HARD, bool GRAD>
+__device__ __forceinline__ void bwd_records_static(const Topo& t, const Corner& C, int k, const Task& T,
+                                                   BwdSmem& S, BwdRec& R, double g, int kind)
+{
+    bwd_records_blob<GRAD>(t, k, T, S, R);
+    bwd_static_gathers<HARD, GRAD>(t, C, R, g, kind);
 }
 
 template <bool HARD, bool GRAD, bool STATIC = false>
@@ -1235,7 +1338,8 @@ __global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_fwd(Topo t, LutSrc ls, Co
     const Corner& C = cs.c[blockIdx.y];
     LutView L;
     if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
-    const Task T = load_task(t, k0 + blockIdx.x);
+    const int k = k0 + blockIdx.x;
+    const Task T = load_task(t, k);
     FwdRec R;
     fwd_records<HARD>(t, T, S, R);
     LSTAMP(1);
@@ -1252,7 +1356,8 @@ __global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_bwd(Topo t, Corners cs, i
     __shared__ BwdSmem S;
     pdl_trigger();
     LSTAMP(0);
-    const Task T = load_task(t, k0 + blockIdx.x);
+    const int k = k0 + blockIdx.x;
+    const Task T = load_task(t, k);
     BwdRec R;
     bwd_records<GRAD>(t, T, S, R);
     LSTAMP(1);
@@ -1543,6 +1648,312 @@ __device__ __forceinline__ void grid_sync(unsigned long long* ctr, unsigned n, u
     grid_wait(ctr, s_target);
 }
 
+
+// ---- per-task record blobs in shared memory (persistent kernel) ---------
+// A block's next task's records (static topology) are fetched by TMA bulk
+// copies (cp.async.bulk, completion on an mbarrier) while the current task
+// computes and the grid barrier drains, so a level starts with its records
+// already in shared memory.
+struct FwdBlob {
+    int4 tk[2];                 // tk_a, tk_b (the Task record)
+    int4 n[2 * (TASK_Q + 1)];
+    int4 q[TASK_Q];
+    int2 a[TASK_Q * 3];
+    uint4 l[TASK_Q * 3];
+    int2 m[TASK_M];
+};
+struct BwdBlob {
+    int4 tk[2];
+    int4 n[2 * (TASK_Q + 1)];
+    int4 m[2 * TASK_M];
+    int4 q[TASK_Q];
+};
+union __align__(16) BlobBuf {
+    FwdBlob f;
+    BwdBlob b;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p)
+{
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(mb)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tWS_MBW:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WS_MBW;\n\t}" :: "r"(smem_u32(mb)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mb)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
+}
+
+// thread 0: fetch task k's forward (bwd = false) or backward records
+__device__ __forceinline__ void issue_blob(const Topo& t, int k, bool bwd, BlobBuf& B, unsigned long long* mb)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of B
+    const size_t kn = (size_t)k * (TASK_Q + 1) * 2;
+    if (!bwd) {
+        mbar_expect_tx(mb, (unsigned)sizeof(FwdBlob));
+        bulk_g2s(&B.f.tk[0], t.tk_a + k, 16, mb);
+        bulk_g2s(&B.f.tk[1], t.tk_b + k, 16, mb);
+        bulk_g2s(B.f.n, t.fb_n + kn, sizeof(B.f.n), mb);
+        bulk_g2s(B.f.q, t.fb_q + (size_t)k * TASK_Q, sizeof(B.f.q), mb);
+        bulk_g2s(B.f.a, t.fb_a + (size_t)k * TASK_Q * 3, sizeof(B.f.a), mb);
+        bulk_g2s(B.f.l, t.fb_l + (size_t)k * TASK_Q * 3, sizeof(B.f.l), mb);
+        bulk_g2s(B.f.m, t.fb_m + (size_t)k * TASK_M, sizeof(B.f.m), mb);
+    } else {
+        mbar_expect_tx(mb, (unsigned)sizeof(BwdBlob));
+        bulk_g2s(&B.b.tk[0], t.tk_a + k, 16, mb);
+        bulk_g2s(&B.b.tk[1], t.tk_b + k, 16, mb);
+        bulk_g2s(B.b.n, t.fb_n + kn, sizeof(B.b.n), mb);
+        bulk_g2s(B.b.m, t.bb_m + (size_t)k * TASK_M * 2, sizeof(B.b.m), mb);
+        bulk_g2s(B.b.q, t.bb_q + (size_t)k * TASK_Q, sizeof(B.b.q), mb);
+    }
+}
+
+__device__ __forceinline__ void nets_from_blob(const int4* n, const Task& T, NetSmem& S)
+{
+    const int i = threadIdx.x;
+    if (i <= T.nq) {
+        const int4 a = n[2 * i], b = n[2 * i + 1];
+        S.aptr[i] = b.y;
+        S.mptr[i] = b.z;
+        if (i < T.nq) {
+            S.root[i] = a.x;
+            S.flags[i] = a.y;
+            S.f0[i] = a.z;
+            S.net[i] = a.w;
+            S.e1[i] = b.x;
+        }
+    }
+}
+
+template <bool HARD>
+__device__ __forceinline__ void fwd_records_smem(const FwdBlob& B, const Task& T, FwdSmem& S, FwdRec& R)
+{
+    nets_from_blob(B.n, T, S.n);
+    const int c = threadIdx.x & 3, qi = threadIdx.x >> 2;
+    const int4 fq = B.q[qi];
+    R.nroot = fq.x;
+    R.nflags = fq.y;
+    R.a0 = fq.z;
+    R.na = fq.w;
+#pragma unroll
+    for (int s = 0; s < FWD_NA; s++) {
+        const int2 fa = B.a[qi * 3 + s];
+        R.from[s] = fa.x;
+        R.arc[s] = fa.y;
+        if (HARD) {
+            const uint4 fl = B.l[qi * 3 + s];
+            const unsigned dw = c < 2 ? fl.x : fl.y, sw = c < 2 ? fl.z : fl.w;
+            R.dl[s] = (unsigned short)((c & 1) ? dw >> 16 : dw & 0xffff);
+            R.sl[s] = (unsigned short)((c & 1) ? sw >> 16 : sw & 0xffff);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) {
+        const int2 fm = B.m[qi + s * TASK_Q];
+        R.mpin[s] = fm.x;
+        R.mfl[s] = fm.y;
+    }
+}
+
+template <bool GRAD>
+__device__ __forceinline__ void bwd_records_smem(const BwdBlob& B, const Task& T, BwdSmem& S, BwdRec& R)
+{
+    nets_from_blob(B.n, T, S.n);
+    const bool late = (threadIdx.x & 3) >= 2;
+    const int qi = threadIdx.x >> 2;
+#pragma unroll
+    for (int s = 0; s < ITEMS; s++) {
+        const int4 m1 = B.m[2 * (qi + s * TASK_Q)], m2 = B.m[2 * (qi + s * TASK_Q) + 1];
+        R.pin[s] = m1.x;
+        R.fl[s] = m1.y;
+        R.o1t[s] = m1.z;
+        R.o1a[s] = m1.w;
+        R.e1[s] = m2.x;
+        R.o0[s] = m2.y;
+        R.no[s] = m2.z;
+        R.arc[s] = (GRAD && late) ? m2.w : -1;
+    }
+    const int4 bq = B.q[qi];
+    R.nroot = bq.x;
+    R.nflags = bq.y;
+    R.ne1 = bq.z;
+}
+
+// a block's task sequence: forward levels 0..L-1, then backward levels
+// L-1..0; within a level tasks lvt_ptr[li] + cta, + ncta, ...
+struct Seq {
+    int step;   // 0 .. 2L-1 (forward levels, then backward levels), 2L = done
+    int k;      // task index or -1 at the end of a level
+};
+__device__ __forceinline__ int seq_level(const Topo& t, int step) { return step < t.L ? step : 2 * t.L - 1 - step; }
+// the first task at or after level position `step` (skipping empty levels)
+__device__ __forceinline__ Seq seq_first(const Topo& t, int step, int cta)
+{
+    for (; step < 2 * t.L; step++) {
+        const int li = seq_level(t, step);
+        const int k = t.lvt_ptr[li] + cta;
+        if (k < t.lvt_ptr[li + 1]) return Seq{step, k};
+    }
+    return Seq{2 * t.L, -1};
+}
+__device__ __forceinline__ Seq seq_next(const Topo& t, Seq s, int cta, int ncta)
+{
+    const int li = seq_level(t, s.step);
+    if (s.k + ncta < t.lvt_ptr[li + 1]) return Seq{s.step, s.k + ncta};
+    return seq_first(t, s.step + 1, cta);
+}
+
+// ---- next task's sweep-static gathers, staged by cp.async -----------------
+// Issued right after the current task's body (addresses from the next
+// task's records, already in smem), they land while the block waits at the
+// grid barrier; afterwards the block only reads them back from smem.  The
+// staged arrays are final for the sweep (RC outputs for the forward sweep,
+// forward outputs for the backward sweep) and are never read through L1
+// before they are final, so the L1-allocating cp.async.ca sees current data.
+struct FwdStage {
+    double mnd[ITEMS][PASS_TPB], mim[ITEMS][PASS_TPB], ld[PASS_TPB];
+};
+struct BwdStage {
+    double ado[ITEMS][PASS_TPB], nd[ITEMS][PASS_TPB], at[ITEMS][PASS_TPB], lse[ITEMS][PASS_TPB],
+        epl[ITEMS][PASS_TPB], wgt[ITEMS][PASS_TPB], epr[ITEMS][PASS_TPB];
+    double n_at[PASS_TPB], n_epr[PASS_TPB], n_lse[PASS_TPB], n_epl[PASS_TPB];
+};
+union __align__(16) StageBuf {
+    FwdStage f;
+    BwdStage b;
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <bool HARD>
+__device__ __forceinline__ void fwd_stage_issue(const Corner& C, const FwdRec& R, FwdStage& st)
+{
+    const int c = threadIdx.x & 3, i = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++)
+        if (R.mpin[k] >= 0) {
+            cp_async8(&st.mnd[k][i], C.net_delay + (size_t)R.mpin[k] * 4 + c);
+            if (HARD) cp_async8(&st.mim[k][i], C.impulse + (size_t)R.mpin[k] * 4 + c);
+        }
+    if (HARD && R.na > 0) cp_async8(&st.ld[i], C.load + (size_t)R.nroot * 4 + c);
+    cp_async_commit();
+}
+
+template <bool HARD>
+__device__ __forceinline__ void fwd_stage_take(const FwdStage& st, FwdRec& R)
+{
+    const int i = threadIdx.x;
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++)
+        if (R.mpin[k] >= 0) {
+            R.mnd[k] = st.mnd[k][i];
+            if (HARD) R.mim[k] = st.mim[k][i];
+        }
+    R.ld = (HARD && R.na > 0) ? st.ld[i] : 0.0;
+}
+
+template <bool HARD, bool GRAD>
+__device__ __forceinline__ void bwd_stage_issue(const Corner& C, const BwdRec& R, BwdStage& st)
+{
+    const int c = threadIdx.x & 3, j = c - 2, i = threadIdx.x;
+    const bool late = c >= 2;
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        if (R.pin[k] >= 0) {
+            const int pin = R.pin[k], fl = R.fl[k];
+            if (HARD) {
+                if (R.o1a[k] >= 0) cp_async8(&st.ado[k][i], C.arc_delay + (size_t)R.o1a[k] * 4 + c);
+                cp_async8(&st.nd[k][i], C.net_delay + (size_t)pin * 4 + c);
+                cp_async8(&st.at[k][i], C.arrival + (size_t)pin * 4 + c);
+                if (!(fl & TM_ROOT) && !(fl & TM_MULTI_EP) && (fl & TM_EP))
+                    cp_async8(&st.epr[k][i], C.ep_required + (size_t)R.e1[k] * 4 + c);
+            }
+            if (GRAD && late && (fl & TM_EP)) {
+                cp_async8(&st.lse[k][i], C.lse_at + (size_t)pin * 2 + j);
+                cp_async8(&st.epl[k][i], C.ep_required + (size_t)R.e1[k] * 4 + 2 + j);
+            }
+        }
+        if (R.arc[k] >= 0) cp_async8(&st.wgt[k][i], C.weights + (size_t)R.arc[k] * 2 + j);
+    }
+    if (R.nroot >= 0) {
+        if (HARD && !(R.nflags & TQ_ROOT_MEMBER)) cp_async8(&st.n_at[i], C.arrival + (size_t)R.nroot * 4 + c);
+        if ((R.nflags & TQ_ROOT_EP) && !(R.nflags & TQ_MULTI_EP)) {
+            if (HARD) cp_async8(&st.n_epr[i], C.ep_required + (size_t)R.ne1 * 4 + c);
+            if (GRAD && late) {
+                cp_async8(&st.n_lse[i], C.lse_at + (size_t)R.nroot * 2 + j);
+                cp_async8(&st.n_epl[i], C.ep_required + (size_t)R.ne1 * 4 + 2 + j);
+            }
+        }
+    }
+    cp_async_commit();
+}
+
+// bwd_static_gathers from the staged values (multi-endpoint pins, rare,
+// still fold their endpoint entries from global memory here)
+template <bool HARD, bool GRAD>
+__device__ __forceinline__ void bwd_stage_take(const Topo& t, const Corner& C, const BwdStage& st,
+                                               BwdRec& R, double g, int kind)
+{
+    const int c = threadIdx.x & 3, j = c - 2, i = threadIdx.x;
+    const bool late = c >= 2;
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < ITEMS; k++) {
+        R.ado[k] = R.nd[k] = R.at[k] = R.lse[k] = R.epl[k] = R.wgt[k] = R.r0[k] = 0.0;
+        if (R.pin[k] >= 0) {
+            const int pin = R.pin[k], fl = R.fl[k];
+            if (HARD) {
+                if (R.o1a[k] >= 0) R.ado[k] = st.ado[k][i];
+                R.nd[k] = st.nd[k][i];
+                R.at[k] = st.at[k][i];
+                if (!(fl & TM_ROOT))
+                    R.r0[k] = (fl & TM_MULTI_EP) ? init_required_multi(t, C, pin, c)
+                                                 : merge_req(c < 2 ? -INF : INF,
+                                                             (fl & TM_EP) ? st.epr[k][i] : (c < 2 ? -INF : INF), c);
+            }
+            if (GRAD && late && (fl & TM_EP)) {
+                R.lse[k] = st.lse[k][i];
+                R.epl[k] = st.epl[k][i];
+            }
+        }
+        if (R.arc[k] >= 0) R.wgt[k] = st.wgt[k][i];
+    }
+    R.n_at = R.n_rr = R.n_seed = 0.0;
+    if (R.nroot >= 0) {
+        const int fq = R.nflags;
+        if (HARD) {
+            if (!(fq & TQ_ROOT_MEMBER)) R.n_at = st.n_at[i];
+            R.n_rr = (fq & TQ_MULTI_EP) ? init_required_multi(t, C, R.nroot, c)
+                                        : merge_req(c < 2 ? -INF : INF,
+                                                    (fq & TQ_ROOT_EP) ? st.n_epr[i] : (c < 2 ? -INF : INF), c);
+        }
+        if (GRAD && late && (fq & TQ_ROOT_EP)) {
+            if (fq & TQ_MULTI_EP) R.n_seed = root_seed(t, C, R.nroot, fq, R.ne1, j, g, kind);
+            else R.n_seed = __dadd_rn(0.0, seed_term(__dsub_rn(st.n_lse[i], st.n_epl[i]), g, kind));
+        }
+    }
+}
+
 union PassSmem {
     FwdSmem f;
     BwdSmem b;
@@ -1578,38 +1989,80 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PassSmem S;
+    __shared__ BlobBuf blob[2];
+    __shared__ __align__(8) unsigned long long mbar[2];
+    // dynamic smem: the staging buffer, then the LUT pool
+    StageBuf& stg = *reinterpret_cast<StageBuf*>(smem);
     const Corner& C = cs.c[blockIdx.y];
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(C.sync_ctr + 2);
     __shared__ unsigned long long s_target;
     const int cta = blockIdx.x, ncta = gridDim.x;
     KSTAMP(0);
-    const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     // pins in no net and the RC of every net ran as ordinary (fully
     // parallel) kernels before this launch: RC is static for the pass
+    Seq cur = seq_first(t, 0, cta);
+    int buf = 0;
+    unsigned phase[2] = {0u, 0u};
+    if (threadIdx.x == 0 && cur.k >= 0) issue_blob(t, cur.k, cur.step >= t.L, blob[0], &mbar[0]);
+    const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem + sizeof(StageBuf), false);
+    KSTAMP(1);
+    Task T{};
+    Seq nxt{2 * t.L, -1};
+    bool fetch_due = false;      // nxt's blob not yet requested
+    // `cur`'s records from its blob and the cp.async of its sweep-static
+    // gathers (right after the previous body, before the grid barrier) ...
+    auto take = [&](bool bwd_rec, FwdRec& RF, BwdRec& RB) {
+        nxt = seq_next(t, cur, cta, ncta);
+        fetch_due = true;
+        mbar_wait(&mbar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        {
+            const int4 a = blob[buf].f.tk[0], b = blob[buf].f.tk[1];   // same offset in both layouts
+            T = Task{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        }
+        if (!bwd_rec) {
+            fwd_records_smem<true>(blob[buf].f, T, S.f, RF);
+            fwd_stage_issue<true>(C, RF, stg.f);
+        } else {
+            bwd_records_smem<GRAD>(blob[buf].b, T, S.b, RB);
+            bwd_stage_issue<true, GRAD>(C, RB, stg.b);
+        }
+    };
+    // ... then (inside the barrier window) the blob fetch of the task after
+    // it into the other buffer
+    auto fetch_next = [&]() {
+        if (fetch_due && threadIdx.x == 0 && nxt.k >= 0)
+            issue_blob(t, nxt.k, nxt.step >= t.L, blob[buf ^ 1], &mbar[buf ^ 1]);
+        fetch_due = false;
+    };
     // ---- forward levels
     {
-        int k = t.lvt_ptr[0] + cta;
-        bool have = t.L > 0 && k < t.lvt_ptr[1];
-        Task T{};
         FwdRec R;
-        KSTAMP(1);
-        if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
+        BwdRec RB_unused;
+        bool have = false;
         for (int li = 0; li < t.L; li++) {
-            const int kend = t.lvt_ptr[li + 1];
             PSTAMP(li, 0);
-            while (have) {
+            while (cur.k >= 0 && cur.step == li) {
+                if (!have) { take(false, R, RB_unused); fetch_next(); }
+                fwd_stage_take<true>(stg.f, R);
                 fwd_body<true, LSE, true>(t, L, C, T, S.f, R, g, li);
-                k += ncta;
-                have = k < kend;
-                if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
+                buf ^= 1;
+                cur = nxt;
+                have = false;
+                if (cur.k >= 0 && cur.step == li) { take(false, R, RB_unused); fetch_next(); have = true; }
             }
+            // the next forward task's records and static-gather issue precede
+            // the arrival; the copies land while the barrier drains
+            if (!have && cur.k >= 0 && cur.step < t.L) { take(false, R, RB_unused); have = true; }
             PSTAMP(li, 1);
             grid_arrive(bar, ncta, &s_target);
-            if (li + 1 < t.L) {          // overlaps the barrier: static data only
-                k = t.lvt_ptr[li + 1] + cta;
-                have = k < t.lvt_ptr[li + 2];
-                if (have) { T = load_task(t, k); fwd_records_static<true>(t, C, T, S.f, R); }
-            }
+            if (have) fetch_next();
             PSTAMP(li, 2);
             grid_wait(bar, &s_target);
         }
@@ -1617,29 +2070,25 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners
     KSTAMP(2);
     // ---- backward levels
     {
-        const int variant = GRAD ? 3 : 1;
-        int li = t.L - 1;
-        int k = li >= 0 ? t.lvt_ptr[li] + cta : 0;
-        bool have = li >= 0 && k < t.lvt_ptr[li + 1];
-        Task T{};
         BwdRec R;
-        if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
-        for (; li >= 0; li--) {
-            const int kend = t.lvt_ptr[li + 1];
+        FwdRec RF_unused;
+        bool have = false;
+        for (int li = t.L - 1; li >= 0; li--) {
+            const int step = 2 * t.L - 1 - li;
             PSTAMP(t.L + li, 0);
-            while (have) {
-                bwd_body<true, GRAD, true>(t, C, T, S.b, R, g, kind, variant, t.L + li);
-                k += ncta;
-                have = k < kend;
-                if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
+            while (cur.k >= 0 && cur.step == step) {
+                if (!have) { take(true, RF_unused, R); fetch_next(); }
+                bwd_stage_take<true, GRAD>(t, C, stg.b, R, g, kind);
+                bwd_body<true, GRAD, true>(t, C, T, S.b, R, g, kind, GRAD ? 3 : 1, t.L + li);
+                buf ^= 1;
+                cur = nxt;
+                have = false;
+                if (cur.k >= 0 && cur.step == step) { take(true, RF_unused, R); fetch_next(); have = true; }
             }
+            if (!have && cur.k >= 0) { take(true, RF_unused, R); have = true; }
             PSTAMP(t.L + li, 1);
             grid_arrive(bar, ncta, &s_target);
-            if (li > 0) {                // overlaps the barrier: static data only
-                k = t.lvt_ptr[li - 1] + cta;
-                have = k < t.lvt_ptr[li];
-                if (have) { T = load_task(t, k); bwd_records_static<true, GRAD>(t, C, T, S.b, R, g, kind); }
-            }
+            if (have) fetch_next();
             PSTAMP(t.L + li, 2);
             grid_wait(bar, &s_target);
         }
@@ -1846,10 +2295,10 @@ struct Launcher {
     void persistent(cudaStream_t s, int w, double g, int kind)
     {
         auto kern = k_pass<Lse, G>;
-        if (lut_bytes > 48 * 1024)
-            WS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_bytes));
+        const size_t dyn = sizeof(StageBuf) + lut_bytes;
+        WS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         int per_sm = 0, dev = 0, n_sm = 0;
-        WS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PASS_TPB, lut_bytes));
+        WS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PASS_TPB, dyn));
         WS_CUDA(cudaGetDevice(&dev));
         WS_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
         int max_tasks = 1;
@@ -1860,7 +2309,7 @@ struct Launcher {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ncta, nc);
         cfg.blockDim = dim3(PASS_TPB);
-        cfg.dynamicSmemBytes = lut_bytes;
+        cfg.dynamicSmemBytes = dyn;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeCooperative;
