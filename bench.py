@@ -167,6 +167,64 @@ def time_reference(raw, max_passes, budget_s):
             "times_ms": [round(1e3 * t, 1) for t in times]}
 
 
+def corner_batch(raw, rank, world, flags, steps, dist=None, n_total=16):
+    """C5: 16 corners of the C3 netlist sharded round-robin
+    over the ranks (corner k -> rank k mod world, 16/world per GPU), all of a
+    rank's corners in ONE ws_run (blockIdx.y = corner), then the batch
+    objective's NCCL exchange: TNS / loss SUM, WNS MIN, d_arc / d_edge SUM
+    (the gradient of sum_k loss_k).  Device time with CUDA events, max over
+    ranks; corners/s is the whole job's."""
+    import torch
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200.corners import combine_local, reduce_batch
+    mine = [k for k in range(n_total) if k % world == rank]
+    nc = len(mine)
+    dev = ws.DeviceDesign(raw, n_corners=nc)
+    for i, k in enumerate(mine):
+        dev.set_values(i, **corner_values(raw, k))
+    stream = torch.cuda.current_stream()
+    d_arc = [dev.tensor("d_arc", i) for i in range(nc)]
+    d_edge = [dev.tensor("d_edge", i) for i in range(nc)]
+    summ = [dev.tensor("summary", i) for i in range(nc)]
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def step():
+        dev.run(flags, corner=0, n_corners=nc, stream=stream)
+        ga, ge = d_arc[0].clone(), d_edge[0].clone()
+        for i in range(1, nc):
+            ga += d_arc[i]
+            ge += d_edge[i]
+        sm = combine_local(summ)
+        if dist is not None:
+            reduce_batch(sm, ga, ge)
+        return sm
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    if dist is not None:
+        dist.barrier()
+    for i in range(steps):
+        flush.fill_(i)
+        evs[i][0].record(stream)
+        sm = step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / steps
+    out = {"workload": "C5: %d corners of the C3 netlist, corner k -> rank k mod N, a rank's "
+                       "corners in one ws_run, NCCL TNS/loss SUM, WNS MIN, d_arc/d_edge SUM" % n_total,
+           "corners_per_gpu": nc, "ms_per_batch": round(ms, 4),
+           "corners_per_s": round(n_total / (ms * 1e-3), 2), "steps": steps,
+           "batch_result": {"tns": float(sm[0]), "wns": float(sm[1]), "loss": float(sm[2])}}
+    dev.close()
+    return out
+
+
 def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     """C4: the timing-driven placement loop — n_inv STA
     fwd+bwd invocations on the C3 netlist with perturbed pin coordinates,
@@ -268,6 +326,8 @@ def main():
     ap.add_argument("--graph", type=int, default=1)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--workload", default="c3", choices=("c1", "c2", "c3"))
+    ap.add_argument("--corners", type=int, default=1,
+                    help="also measure the C5 16-corner batch (corner_batch key); 0: skip")
     ap.add_argument("--placement", type=int, default=200,
                     help="C4 placement-loop invocations reported under placement_loop (0: skip)")
     args = ap.parse_args()
@@ -441,6 +501,10 @@ def main():
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / ke / world
 
+    cb = None
+    if args.corners and 16 % world == 0:
+        cb = corner_batch(raw, rank, world, flags, steps=max(3, min(args.steps, 10)), dist=dist)
+
     if rank == 0:
         P, M, N, A, I, E = (dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep)
         B = algorithmic_bytes(P, M, N, A, I, E)
@@ -475,6 +539,8 @@ def main():
                 "clocks": clk.summary(),
                 "result": {"tns": tns, "wns": wns, "loss": loss},
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
+        if cb is not None:
+            line["corner_batch"] = cb
         if args.placement and world == 1:
             line["placement_loop"] = placement_loop(raw, n_inv=args.placement)
         if args.cpu_baseline and world == 1:

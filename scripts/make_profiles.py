@@ -26,7 +26,7 @@ if os.path.exists(lc):
                  "# per-launch times are cold-cache and serialised: compare shares, not absolutes\n")
         fh.write(out)
     shutil.copy(lc, os.path.join(P, f"launches_{R}.csv"))
-for k in ("fwd", "bwd", "rc"):
+for k in ("fwd", "bwd", "rc", "pglevel", "pgmem", "wire"):
     rep = os.path.join(G, f"prof_{k}_{R}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -37,4 +37,43 @@ for k in ("fwd", "bwd", "rc"):
         fh.write(s)
         fh.write("\n# --page details\n")
         fh.write(d)
+# placement step: the last step's launches (wire + pass + position gradients)
+pc = os.path.join(G, f"place_launches_{R}.csv")
+if os.path.exists(pc):
+    import collections
+    import csv
+    rows = list(csv.reader(open(pc)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, ii, mi, vi, ui = (h.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value", "Metric Unit"))
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        d = per.setdefault(int(r[ii]), {"name": r[ki].split("(")[0].replace("(anonymous namespace)::", "")})
+        v = float(r[vi].replace(",", ""))
+        u = r[ui]
+        if r[mi] == "gpu__time_duration.sum":
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
+        elif u in ("Kbyte", "Mbyte", "Gbyte", "byte", "KB", "MB", "GB", "B"):
+            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}[u]
+        d[r[mi]] = v
+    ids = list(per)
+    wire = [i for i in ids if per[i]["name"].endswith("k_wire")]
+    last = [per[i] for i in ids if i >= wire[-1]] if wire else []
+    agg = collections.OrderedDict()
+    for d in last:
+        a = agg.setdefault(d["name"], [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += d.get("gpu__time_duration.sum", 0.0)
+        a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    tot = sum(a[1] for a in agg.values()) or 1.0
+    with open(os.path.join(P, f"place_launches_{R}.txt"), "w") as fh:
+        fh.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum\n"
+                 "#   --clock-control none, python scripts/place_step.py 2: the second C3 placement step\n"
+                 "# (k_wire -> pass -> position gradients); cold-cache serialised: read shares\n")
+        fh.write(f"{len(last)} launches, {tot:.1f} us total\n")
+        for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            fh.write(f"{k[:44]:44s} n={n:4d} total={t:9.1f}us avg={t / n:8.2f}us share={t / tot:.3f} "
+                     f"dram={b / 1e6:9.2f}MB\n")
 print(sorted(os.listdir(P)))
