@@ -369,11 +369,19 @@ def main():
         return 0
 
     import torch
+    # WS_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo, so
+    # the N>1 path can be exercised on a one-GPU box
+    share = os.environ.get("WS_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2603_28381_b200 as ws
     from paper_2603_28381_b200 import _lib
     from paper_2603_28381_b200.corners import reduce_batch
