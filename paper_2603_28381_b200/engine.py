@@ -78,6 +78,12 @@ class DeviceDesign:
         self.clock_period = raw.clock_period
 
     # -- lifetime ---------------------------------------------------------
+    @classmethod
+    def from_file(cls, path: str, n_corners: int = 1, verify: bool = True) -> "DeviceDesign":
+        """Ingest a design written by ingest.save_raw (hash-verified)."""
+        from .ingest import load_raw
+        return cls(load_raw(path, verify=verify), n_corners=n_corners)
+
     def close(self):
         if getattr(self, "_h", None):
             lib().ws_destroy(self._h)
