@@ -29,6 +29,31 @@ namespace {
 
 constexpr double INF = __builtin_huge_val();
 
+// Programmatic dependent launch between the sweep's kernels: each kernel
+// loads its records and every pass output it needs (final before the sweep
+// began), then waits for its predecessor and only then lets its successor
+// start.  A kernel's prologue therefore overlaps the previous kernel's body
+// and may read anything written two or more launches earlier.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    WS_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 __device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
 {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
@@ -166,7 +191,11 @@ __global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, Corner C, 
                                                 int u_begin, int n2)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n2) return;
+    if (i >= n2) {
+        pdl_wait();
+        pdl_trigger();
+        return;
+    }
     const int u = u_begin + (i >> 1), j = i & 1, c = 2 + j;
     const int pin = t.tm_pin[u], o1 = t.tm_o1_arc[u], fl = t.tm_flags[u];
     const int f = pt.tm_f[u], root = pt.tm_root[u];
@@ -175,6 +204,8 @@ __global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, Corner C, 
     const double sr = C.slew[(size_t)root * 4 + c];
     const double rr = C.mem_res[(size_t)f * 4 + c], cp = C.mem_cap[(size_t)f * 4 + c];
     const double d = C.net_delay[(size_t)pin * 4 + c], adj = C.adjoint[(size_t)pin * 2 + j];
+    pdl_wait();          // gsa / gsr of the higher levels
+    pdl_trigger();
     double g = 0.0;
     if (o1 >= 0) {
         g = __dadd_rn(g, G.gsa[(size_t)o1 * 2 + j]);
@@ -211,7 +242,11 @@ __global__ void __launch_bounds__(PG_WARPS * 32, 3) k_pg_level(Topo t, LutSrc ls
     const int lane = threadIdx.x & 31, grp = lane / PG_G, j = lane & 1, c = 2 + j;
     const int slot = (lane % PG_G) >> 1;
     const int wq = (blockIdx.x * PG_WARPS + (threadIdx.x >> 5)) * (32 / PG_G);
-    if (wq >= nq) return;                        // whole warp idle
+    if (wq >= nq) {                              // whole warp idle
+        pdl_wait();
+        pdl_trigger();
+        return;
+    }
     const int qi = wq + grp;
     const bool act = qi < nq;
     // ---- hop 1: level-major task records of the group's net
@@ -247,6 +282,8 @@ __global__ void __launch_bounds__(PG_WARPS * 32, 3) k_pg_level(Topo t, LutSrc ls
         return r;
     };
     const Arc arc0 = load_arc(slot);
+    pdl_wait();          // this level's k_pg_mem (member terms), higher levels' gsa
+    pdl_trigger();
     // ---- root-slew terms of the members (k_pg_mem), summed in slot order
     const double* __restrict__ sct = G.sc_t;
     double part = 0.0;
@@ -330,6 +367,8 @@ __device__ __forceinline__ double sgn(double d) { return d > 0.0 ? 1.0 : (d < 0.
 __global__ void k_pg_len(int M, const int* __restrict__ mem_pin, const int* __restrict__ parent_pin,
                          PlaceCorner G)
 {
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= M) return;
     const double* w = G.wire;
@@ -351,6 +390,8 @@ __global__ void k_pg_xy(int P, const int* __restrict__ member_of_pin, const int*
                         const int* __restrict__ pc_mem, const double2* __restrict__ e,
                         double2* __restrict__ d_xy)
 {
+    pdl_wait();
+    pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
     const int own = member_of_pin[p];
@@ -514,26 +555,32 @@ int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s)
         // arcs of lower-level targets are read before written: start from 0
         if (t.A) WS_CUDA(cudaMemsetAsync(g.gsa, 0, sizeof(double) * 2 * (size_t)t.A, s));
         if (t.P) WS_CUDA(cudaMemsetAsync(g.gsr, 0, sizeof(double) * 2 * (size_t)t.P, s));
+        bool pdl = false;        // the first sweep kernel waits for the whole pass
         for (int li = t.L - 1; li >= 0; li--) {
             const int q0 = ctx.lv_ptr_host[li], nq = ctx.lv_ptr_host[li + 1] - q0;
             if (nq <= 0) continue;
             const int ub = ctx.pt.tq_mptr_host[q0], un = ctx.pt.tq_mptr_host[q0 + nq] - ub;
             if (un > 0) {
-                k_pg_mem<<<(2 * un + 255) / 256, 256, 0, s>>>(t, ctx.pt, d, g, ub, 2 * un);
+                launch_pdl(pdl, k_pg_mem, dim3((2 * un + 255) / 256), dim3(256), 0, s, t, ctx.pt, d, g, ub,
+                           2 * un);
+                pdl = true;
                 count++;
             }
-            k_pg_level<<<(nq + PG_WARPS * (32 / PG_G) - 1) / (PG_WARPS * (32 / PG_G)), PG_WARPS * 32, lut_bytes, s>>>(
-                t, ls, use_smem, d, g, q0, nq);
+            launch_pdl(pdl, k_pg_level, dim3((nq + PG_WARPS * (32 / PG_G) - 1) / (PG_WARPS * (32 / PG_G))),
+                       dim3(PG_WARPS * 32), lut_bytes, s, t, ls, use_smem, d, g, q0, nq);
+            pdl = true;
             count++;
         }
         if (t.M) {
-            k_pg_len<<<(t.M + 255) / 256, 256, 0, s>>>(t.M, t.mem_pin, ctx.pt.parent_pin, g);
+            launch_pdl(pdl, k_pg_len, dim3((t.M + 255) / 256), dim3(256), 0, s, t.M,
+                       (const int*)t.mem_pin, (const int*)ctx.pt.parent_pin, g);
+            pdl = true;
             count++;
         }
         if (t.P) {
-            k_pg_xy<<<(t.P + 255) / 256, 256, 0, s>>>(
-                t.P, t.member_of_pin, ctx.pt.pc_ptr, ctx.pt.pc_mem,
-                reinterpret_cast<const double2*>(g.sc_buf), reinterpret_cast<double2*>(g.d_xy));
+            launch_pdl(pdl, k_pg_xy, dim3((t.P + 255) / 256), dim3(256), 0, s, t.P,
+                       (const int*)t.member_of_pin, (const int*)ctx.pt.pc_ptr, (const int*)ctx.pt.pc_mem,
+                       reinterpret_cast<const double2*>(g.sc_buf), reinterpret_cast<double2*>(g.d_xy));
             count++;
         }
         WS_CHECK_LAUNCH();
