@@ -210,11 +210,12 @@ __device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
     if (n > 1) {
         int lo;
         if (n <= 8) {
-            // upper_bound on a sorted axis = number of entries <= q: a fixed,
-            // branch-free count instead of the data-dependent search loop
+            // upper_bound on a sorted axis = number of entries <= q (a
+            // monotone prefix): four fixed branch-free halving steps
             lo = 0;
 #pragma unroll
-            for (int k = 0; k < 8; k++) lo += (k < n && ax[k] <= q) ? 1 : 0;
+            for (int s = 8; s >= 1; s >>= 1)
+                if (lo + s <= n && ax[lo + s - 1] <= q) lo += s;
         } else {
             lo = upper_bound_long(ax, n, q);
         }

@@ -736,7 +736,13 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
                         if (k < R.na && (k == 0 || x[k] > cm)) cm = x[k];     // np.maximum.reduceat
                     }
 #pragma unroll
-                    for (int k = 0; k < FWD_NA; k++) z[k] = exp(__ddiv_rn(__dsub_rn(x[k], cm), g));
+                    for (int k = 0; k < FWD_NA; k++) {
+                        // the max element gives exactly +0 / g = +0 and
+                        // exp(+0) = 1: skip the division, whose zero
+                        // dividend would take the IEEE slow path
+                        const double dx = __dsub_rn(x[k], cm);
+                        z[k] = dx == 0.0 ? 1.0 : exp(__ddiv_rn(dx, g));
+                    }
                     double rest = 0.0;
 #pragma unroll
                     for (int k = 1; k < FWD_NA; k++)
