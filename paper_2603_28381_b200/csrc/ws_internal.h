@@ -137,6 +137,7 @@ struct Context {
     std::vector<int> graph_launches;  // kernels per captured graph
     PlaceTopo pt;
     std::vector<PlaceCorner> place;   // per corner once place_enable ran
+    std::vector<cudaEvent_t> pg_events;   // [L + 2]: per backward level, fork, join
 };
 
 void build_topology(Context& ctx, const ws_design_desc* d);
@@ -153,7 +154,11 @@ void launch_perturb(const Context& ctx, int dst, int src, unsigned long long see
                     cudaStream_t s);
 void place_enable(Context& ctx);
 int launch_wire(Context& ctx, int c0, int nc, cudaStream_t s);
-int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s);
+// position-gradient sweep; with `bwd_done` (one event per level, recorded
+// after that level's backward kernel on the pass stream) it runs on stream
+// `gs` and level l starts as soon as the pass's backward level l is done
+int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s, cudaStream_t gs = nullptr,
+                   const std::vector<cudaEvent_t>* bwd_done = nullptr);
 void summary_plan_init(Context& ctx);
 void summary_plan_free(Context& ctx);
 void topo_field_to_host(Context& ctx, int field, int64_t* dst);

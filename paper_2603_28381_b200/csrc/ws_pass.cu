@@ -2340,7 +2340,8 @@ struct Launcher {
 };
 
 void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind, int gran,
-               cudaStream_t s, cudaStream_t gs, int w, int& count)
+               cudaStream_t s, cudaStream_t gs, int w, int& count,
+               const std::vector<cudaEvent_t>* bwd_done = nullptr)
 {
     const int L = ctx.t.L;
     Launcher la(ctx, c0, nc);
@@ -2361,7 +2362,10 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         la.free_pins(s, true);
         la.rc(s, w);
         for (int li = 0; li < L; li++) la.fwd<true, true>(s, li, g);
-        for (int li = L - 1; li >= 0; li--) la.bwd<true, true>(s, li, g, kind);
+        for (int li = L - 1; li >= 0; li--) {
+            la.bwd<true, true>(s, li, g, kind);
+            if (bwd_done) WS_CUDA(cudaEventRecord((*bwd_done)[li], s));
+        }
         la.fin(s, g, kind);
         la.summary(s, g, kind, true, true);
     } else if (two) {
@@ -2430,10 +2434,32 @@ void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int lo
 {
     int count = 0;
     if (flags & WS_RUN_WIRE) count += launch_wire(ctx, c0, nc, s);
+    // the position-gradient sweep overlaps the backward sweep on the second
+    // stream (fused single-chunk passes): level l waits only for backward level l
+    const bool overlap = (flags & WS_RUN_POSGRAD) && (flags & WS_RUN_FUSED) && nc <= MAXC &&
+                         !(flags & WS_RUN_PERSISTENT) && ctx.t.L > 0;
+    std::vector<cudaEvent_t>& ev = ctx.pg_events;
+    if (overlap) {
+        while ((int)ev.size() < ctx.t.L + 2) {
+            cudaEvent_t e;
+            WS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+        }
+        WS_CUDA(cudaEventRecord(ev[ctx.t.L], s));          // fork: after everything queued on s
+        WS_CUDA(cudaStreamWaitEvent(gs, ev[ctx.t.L], 0));
+    }
     for (int k = 0; k < nc; k += MAXC)
         run_chunk(ctx, c0 + k, std::min(MAXC, nc - k), flags, gamma, loss_kind, granularity, s, gs,
-                  w, count);
-    if (flags & WS_RUN_POSGRAD) count += launch_posgrad(ctx, c0, nc, s);
+                  w, count, overlap ? &ev : nullptr);
+    if (flags & WS_RUN_POSGRAD) {
+        if (overlap) {
+            count += launch_posgrad(ctx, c0, nc, s, gs, &ev);
+            WS_CUDA(cudaEventRecord(ev[ctx.t.L + 1], gs));  // join
+            WS_CUDA(cudaStreamWaitEvent(s, ev[ctx.t.L + 1], 0));
+        } else {
+            count += launch_posgrad(ctx, c0, nc, s);
+        }
+    }
     ctx.launches_last_run = count;
 }
 

@@ -539,8 +539,15 @@ int launch_wire(Context& ctx, int c0, int nc, cudaStream_t s)
     return nc;
 }
 
-int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s)
+int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s_pass, cudaStream_t gs,
+                   const std::vector<cudaEvent_t>* bwd_done)
 {
+    // with bwd_done the sweep runs on gs; every PG_GROUP levels it waits for
+    // the pass's backward level at the group's bottom (which implies the
+    // group's upper levels), and the kernel after each wait is launched
+    // without PDL so its prologue cannot run ahead of that dependency
+    constexpr int PG_GROUP = 4;
+    const cudaStream_t s = bwd_done ? gs : s_pass;
     const Topo& t = ctx.t;
     int count = 0;
     const LutSrc ls{t.lut_s_ptr, t.lut_l_ptr, t.lut_t_ptr, t.lut_s_flat, t.lut_l_flat, t.NL,
@@ -556,8 +563,14 @@ int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s)
         if (t.A) WS_CUDA(cudaMemsetAsync(g.gsa, 0, sizeof(double) * 2 * (size_t)t.A, s));
         if (t.P) WS_CUDA(cudaMemsetAsync(g.gsr, 0, sizeof(double) * 2 * (size_t)t.P, s));
         bool pdl = false;        // the first sweep kernel waits for the whole pass
+        int waited = t.L;        // lowest backward level known complete
         for (int li = t.L - 1; li >= 0; li--) {
             const int q0 = ctx.lv_ptr_host[li], nq = ctx.lv_ptr_host[li + 1] - q0;
+            if (bwd_done && li < waited) {
+                waited = std::max(0, li - PG_GROUP + 1);
+                WS_CUDA(cudaStreamWaitEvent(s, (*bwd_done)[waited], 0));
+                pdl = false;
+            }
             if (nq <= 0) continue;
             const int ub = ctx.pt.tq_mptr_host[q0], un = ctx.pt.tq_mptr_host[q0 + nq] - ub;
             if (un > 0) {
