@@ -127,8 +127,10 @@ enum ws_run_flags {
     WS_RUN_PERSISTENT = 256u,/* with HARD (and LSE|GRAD): the whole pass as one cooperative
                                 kernel, grid barrier between levels */
     WS_RUN_WIRE = 512u,      /* first: mem_res / mem_cap from the positions (WS_V_XY ...) */
-    WS_RUN_POSGRAD = 1024u   /* last (needs HARD|LSE|GRAD in the same call): slew / load
+    WS_RUN_POSGRAD = 1024u,  /* last (needs HARD|LSE|GRAD in the same call): slew / load
                                 adjoint sweep, Elmore adjoint, dL/dxy */
+    WS_RUN_TIMED = 2048u     /* sequential mode only: a CUDA event after every launch, read
+                                back with ws_kernel_times (measured KernelGraph costs) */
 };
 
 enum ws_loss_kind { WS_LOSS_HINGE = 0, WS_LOSS_SOFTPLUS = 1 };
@@ -172,6 +174,13 @@ int ws_summary(ws_ctx *ctx, int corner, double *out, void *stream);
 int ws_set_probe(ws_ctx *ctx, void *device_buf);
 /* number of kernels launched by the last ws_run */
 int ws_last_launch_count(ws_ctx *ctx);
+/* Per-launch device times of the last WS_RUN_TIMED run (synchronizes):
+ * kind[i] in {0 net_rc, 1 cell_delay_at, 2 slack_bwd, 3 lse_fwd, 4 grad_bwd,
+ * 5 other} and level[i] as in fusion.py:113-160 build_kernel_graph, ms[i] the
+ * time since the previous mark.  Returns the number of entries (<= cap), or
+ * -1 on error.  Feeds fusion.measured_kernel_costs -> schedule_fused
+ * (fusion.py:216-249), the makespan model the reference simulates. */
+int ws_kernel_times(ws_ctx *ctx, int *kind, int *level, float *ms, int cap);
 
 /* Legacy per-level shims with the reference's raw kernel semantics
  * (int64 indices, float64 values, host buffers, outputs updated in place). */

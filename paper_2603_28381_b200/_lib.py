@@ -46,7 +46,7 @@ TOPO = {name: i for i, name in enumerate(TOPO_FIELDS)}
 RUN_HARD, RUN_LSE, RUN_GRAD, RUN_TWO_STREAM, RUN_FUSED, RUN_GRAPH, RUN_SUMMARY, RUN_SLACK = (
     1, 2, 4, 8, 16, 32, 64, 128)
 RUN_PERSISTENT = 256
-RUN_WIRE, RUN_POSGRAD = 512, 1024
+RUN_WIRE, RUN_POSGRAD, RUN_TIMED = 512, 1024, 2048
 LOSS_KINDS = {"hinge": 0, "softplus": 1}
 DIMS_LEN = 11
 
@@ -55,7 +55,7 @@ EXPORTS = ("ws_abi_version", "ws_last_error", "ws_last_error_pin", "ws_create", 
            "ws_dims", "ws_topology_len", "ws_get_topology", "ws_set_values",
            "ws_perturb_values", "ws_run", "ws_get", "ws_device_ptr", "ws_value_ptr",
            "ws_summary", "ws_last_launch_count", "ws_set_state", "ws_set_probe", "ws_rc_level", "ws_forward_level",
-           "ws_backward_level")
+           "ws_backward_level", "ws_kernel_times")
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_i32p = ctypes.POINTER(ctypes.c_int32)
@@ -122,6 +122,8 @@ def lib():
     L.ws_value_ptr.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp), _c_i64p]
     L.ws_summary.argtypes = [_vp, ctypes.c_int, _c_f64p, _vp]
     L.ws_last_launch_count.argtypes = [_vp]
+    _ip = ctypes.POINTER(ctypes.c_int)
+    L.ws_kernel_times.argtypes = [_vp, _ip, _ip, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.ws_set_probe.argtypes = [_vp, _vp]
     i64, vp, d = ctypes.c_int64, _vp, ctypes.c_double
     L.ws_rc_level.argtypes = [i64, vp, i64, vp, vp, vp, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp,

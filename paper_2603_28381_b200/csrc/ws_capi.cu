@@ -273,6 +273,8 @@ void ws_destroy(ws_ctx* h)
     cudaDeviceSynchronize();
     for (auto& g : c.graphs) cudaGraphExecDestroy(g.exec);
     for (auto e : c.events) cudaEventDestroy(e);
+    for (auto e : c.pg_events) cudaEventDestroy(e);
+    for (auto e : c.timed_events) cudaEventDestroy(e);
     ws::summary_plan_free(c);
     c.val_mem.release();
     c.topo_mem.release();
@@ -372,6 +374,9 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
         const unsigned need = WS_RUN_HARD | WS_RUN_LSE | WS_RUN_GRAD;
         if ((flags & WS_RUN_POSGRAD) && (flags & need) != need)
             throw ws::Error(WS_ERR_STATE, "WS_RUN_POSGRAD needs HARD|LSE|GRAD in the same run");
+        if ((flags & WS_RUN_TIMED) &&
+            (flags & (WS_RUN_FUSED | WS_RUN_TWO_STREAM | WS_RUN_PERSISTENT | WS_RUN_GRAPH)))
+            throw ws::Error(WS_ERR_VALUE, "WS_RUN_TIMED needs the sequential mode without graph capture");
         if ((flags & WS_RUN_POSGRAD) && (flags & WS_RUN_PERSISTENT))
             throw ws::Error(WS_ERR_VALUE, "WS_RUN_POSGRAD is not available with WS_RUN_PERSISTENT");
         if (flags & (WS_RUN_WIRE | WS_RUN_POSGRAD)) ws::place_enable(c);
@@ -482,6 +487,25 @@ int ws_summary(ws_ctx* h, int corner, double* out, void* stream)
 }
 
 int ws_last_launch_count(ws_ctx* h) { return h ? h->c.launches_last_run : -1; }
+
+int ws_kernel_times(ws_ctx* h, int* kind, int* level, float* ms, int cap)
+{
+    int n = -1;
+    const int rc = guarded([&] {
+        if (!h || (cap > 0 && (!kind || !level || !ms))) throw ws::Error(WS_ERR_VALUE, "null argument");
+        ws::Context& c = h->c;
+        n = std::max(0, std::min(cap, c.timed_n - 1));
+        if (c.timed_n > 0) WS_CUDA(cudaEventSynchronize(c.timed_events[c.timed_n - 1]));
+        for (int i = 0; i < n; i++) {
+            float t = 0.f;
+            WS_CUDA(cudaEventElapsedTime(&t, c.timed_events[i], c.timed_events[i + 1]));
+            kind[i] = c.timed_kind[i + 1];
+            level[i] = c.timed_level[i + 1];
+            ms[i] = t;
+        }
+    });
+    return rc == WS_OK ? n : -1;
+}
 
 int ws_set_probe(ws_ctx* h, void* device_buf)
 {

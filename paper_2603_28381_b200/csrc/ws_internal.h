@@ -138,6 +138,11 @@ struct Context {
     PlaceTopo pt;
     std::vector<PlaceCorner> place;   // per corner once place_enable ran
     std::vector<cudaEvent_t> pg_events;   // [L + 2]: per backward level, fork, join
+    // WS_RUN_TIMED: an event after every launch of a sequential pass, tagged
+    // with the reference's kernel kind and level (fusion.py:113-160)
+    std::vector<cudaEvent_t> timed_events;
+    std::vector<int> timed_kind, timed_level;
+    int timed_n = 0;
 };
 
 void build_topology(Context& ctx, const ws_design_desc* d);

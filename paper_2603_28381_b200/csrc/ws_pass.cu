@@ -2221,6 +2221,24 @@ struct Launcher {
         if (!use_smem) lut_bytes = 0;
     }
     dim3 grid1(int n, int tpb) const { return dim3((unsigned)std::max(1, (n + tpb - 1) / tpb), nc); }
+    // WS_RUN_TIMED: an event after the launch just issued, tagged (kind, level)
+    bool timed = false;
+    void mark(cudaStream_t s, int kind, int level)
+    {
+        if (!timed) return;
+        auto& ev = ctx.timed_events;
+        if ((int)ev.size() <= ctx.timed_n) {
+            cudaEvent_t e;
+            WS_CUDA(cudaEventCreate(&e));
+            ev.push_back(e);
+            ctx.timed_kind.push_back(0);
+            ctx.timed_level.push_back(0);
+        }
+        WS_CUDA(cudaEventRecord(ev[ctx.timed_n], s));
+        ctx.timed_kind[ctx.timed_n] = kind;
+        ctx.timed_level[ctx.timed_n] = level;
+        ctx.timed_n++;
+    }
     int tasks(int li) const { return ctx.lvt_ptr_host[li + 1] - ctx.lvt_ptr_host[li]; }
 
     void free_pins(cudaStream_t s, bool lse)
@@ -2404,24 +2422,44 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         WS_CUDA(cudaStreamWaitEvent(s, ev[n_groups + 1], 0));
         la.summary(s, g, kind, grad, true);
     } else {
+        // kinds of fusion.py's KernelGraph: 0 net_rc, 1 cell_delay_at,
+        // 2 slack_bwd, 3 lse_fwd, 4 grad_bwd, 5 other
+        la.timed = flags & WS_RUN_TIMED;
+        la.mark(s, 5, -1);                       // start
         if (hard) {
             la.free_pins(s, lse);
-            la.rc(s, w);
-            for (int li = 0; li < L; li++) la.fwd<true, false>(s, li, g);
+            la.mark(s, 5, -1);
+            la.rc(s, w);                         // one launch: the RC of every level
+            la.mark(s, 0, 0);
+            for (int li = 0; li < L; li++) {
+                la.fwd<true, false>(s, li, g);
+                la.mark(s, 1, li);
+            }
         }
         if (lse) {
             if (!hard) la.lse_seed(s);
-            for (int li = 0; li < L; li++) la.fwd<false, true>(s, li, g);
+            for (int li = 0; li < L; li++) {
+                la.fwd<false, true>(s, li, g);
+                la.mark(s, 3, li);
+            }
         }
         if (hard)
-            for (int li = L - 1; li >= 0; li--) la.bwd<true, false>(s, li, g, kind);
+            for (int li = L - 1; li >= 0; li--) {
+                la.bwd<true, false>(s, li, g, kind);
+                la.mark(s, 2, li);
+            }
         if (grad) {
-            for (int li = L - 1; li >= 0; li--) la.bwd<false, true>(s, li, g, kind);
+            for (int li = L - 1; li >= 0; li--) {
+                la.bwd<false, true>(s, li, g, kind);
+                la.mark(s, 4, li);
+            }
             la.fin(s, g, kind);
+            la.mark(s, 5, -1);
         }
         if (!hard && (flags & WS_RUN_SLACK)) la.slack_all(s);
         if (hard || grad || (flags & WS_RUN_SUMMARY))
             la.summary(s, g, kind, grad, hard || (flags & WS_RUN_SUMMARY));
+        la.mark(s, 5, -1);
     }
     WS_CHECK_LAUNCH();
     count += la.count;
@@ -2433,6 +2471,7 @@ void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int lo
               int granularity, cudaStream_t s, cudaStream_t gs, int w)
 {
     int count = 0;
+    ctx.timed_n = 0;
     if (flags & WS_RUN_WIRE) count += launch_wire(ctx, c0, nc, s);
     // the position-gradient sweep overlaps the backward sweep on the second
     // stream (fused single-chunk passes): level l waits only for backward level l

@@ -169,6 +169,17 @@ class DeviceDesign:
     def last_launch_count(self) -> int:
         return int(lib().ws_last_launch_count(self._h))
 
+    def kernel_times(self):
+        """[(kind, level, ms)] of the last RUN_TIMED pass (fusion.py kinds)."""
+        cap = 8 * (self.n_levels + 4)
+        kind = (ctypes.c_int * cap)()
+        level = (ctypes.c_int * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = lib().ws_kernel_times(self._h, kind, level, ms, cap)
+        if n < 0:
+            check(_lib.WS_ERR_VALUE)
+        return [(int(kind[i]), int(level[i]), float(ms[i])) for i in range(n)]
+
     # -- results -------------------------------------------------------------------
     def _shape(self, name):
         if name in ("load", "net_delay", "impulse", "slew", "arrival", "required", "slack"):

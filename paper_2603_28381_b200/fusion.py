@@ -90,6 +90,28 @@ class KernelGraph:
     def cross_deps(self, kid: str) -> list:
         return [e.src for e in self.edges if e.dst == kid]
 
+    def is_acyclic(self) -> bool:
+        """Kahn over stream orders + event edges (fusion.py KernelGraph)."""
+        succ = {k: [] for k in self.kernels}
+        indeg = {k: 0 for k in self.kernels}
+        for order in (self.sta_order, self.grad_order):
+            for a, b in zip(order, order[1:]):
+                succ[a].append(b)
+                indeg[b] += 1
+        for e in self.edges:
+            succ[e.src].append(e.dst)
+            indeg[e.dst] += 1
+        ready = [k for k, d in indeg.items() if d == 0]
+        seen = 0
+        while ready:
+            k = ready.pop()
+            seen += 1
+            for n in succ[k]:
+                indeg[n] -= 1
+                if indeg[n] == 0:
+                    ready.append(n)
+        return seen == len(self.kernels)
+
 
 def build_kernel_graph(schedule, costs=None, granularity: int = 10) -> KernelGraph:
     """The stream/event structure the two-stream executor launches
@@ -135,6 +157,181 @@ def build_kernel_graph(schedule, costs=None, granularity: int = 10) -> KernelGra
         edges.append(EventEdge(f"slack_bwd:{n_levels - 1}", f"grad_bwd:{n_levels - 1}"))
     return KernelGraph(kernels=kernels, edges=edges, sta_order=sta_order, grad_order=grad_order,
                        event_granularity=granularity, n_levels=n_levels)
+
+
+# ---------------------------------------------------------------------------
+# makespan model (fusion.py:163-265): the reference's two-lane schedule over
+# per-kernel costs.  Here the costs can be MEASURED on the device
+# (measured_kernel_costs), which validates the model against the real
+# two-stream run (makespan_report).
+
+@dataclass
+class ScheduleResult:
+    records: list
+    makespan: float
+    overlap_fraction: float
+    sta_finish: float
+    grad_cycles: float
+    overlapped_grad_cycles: float
+
+    def _times(self):
+        got = getattr(self, "_times_cache", None)
+        if got is None:
+            got = {r["id"]: (r["start"], r["finish"]) for r in self.records}
+            self._times_cache = got
+        return got
+
+    def start(self, kid):
+        return self._times()[kid][0]
+
+    def finish(self, kid):
+        return self._times()[kid][1]
+
+
+def _result(graph: KernelGraph, times: dict) -> ScheduleResult:
+    records, sta_fin = [], 0.0
+    for kid in graph.sta_order + graph.grad_order:
+        k = graph.kernels[kid]
+        s, f = times[kid]
+        records.append({"id": kid, "stream": k.stream, "kind": k.kind, "level": k.level,
+                        "start": s, "finish": f})
+        if k.stream == STA_STREAM:
+            sta_fin = max(sta_fin, f)
+    grad = sum(r["finish"] - r["start"] for r in records if r["stream"] == GRAD_STREAM)
+    over = sum(max(0.0, min(r["finish"], sta_fin) - r["start"]) for r in records
+               if r["stream"] == GRAD_STREAM)
+    return ScheduleResult(records=records, makespan=max((f for _, f in times.values()), default=0.0),
+                          overlap_fraction=over / grad if grad > 0 else 0.0, sta_finish=sta_fin,
+                          grad_cycles=grad, overlapped_grad_cycles=over)
+
+
+def schedule_sequential(graph: KernelGraph) -> ScheduleResult:
+    """One lane: the sta stream's kernels, then the grad stream's."""
+    times, t = {}, 0.0
+    for kid in graph.sta_order + graph.grad_order:
+        c = graph.kernels[kid].cost
+        times[kid] = (t, t + c)
+        t += c
+    return _result(graph, times)
+
+
+def schedule_fused(graph: KernelGraph, contention: float = 1.0) -> ScheduleResult:
+    """Two lanes: the sta lane never waits; a grad kernel starts when its lane
+    is free and its event sources finished, at `contention` x cost while the
+    sta lane is still busy."""
+    times, t = {}, 0.0
+    for kid in graph.sta_order:
+        c = graph.kernels[kid].cost
+        times[kid] = (t, t + c)
+        t += c
+    sta_total, t = t, 0.0
+    for kid in graph.grad_order:
+        start = max([t] + [times[d][1] for d in graph.cross_deps(kid)])
+        c = graph.kernels[kid].cost * (contention if start < sta_total else 1.0)
+        times[kid] = (start, start + c)
+        t = start + c
+    return _result(graph, times)
+
+
+def check_schedule(graph: KernelGraph, result: ScheduleResult) -> list:
+    """Stream order, event edges, makespan = last finish."""
+    problems = []
+    for order in (graph.sta_order, graph.grad_order):
+        for a, b in zip(order, order[1:]):
+            if result.start(b) < result.finish(a):
+                problems.append(f"stream order violated: {b} starts before {a} ends")
+    for e in graph.edges:
+        if result.start(e.dst) < result.finish(e.src):
+            problems.append(f"event violated: {e.dst} starts before {e.src} ends")
+    last = max((r["finish"] for r in result.records), default=0.0)
+    if result.makespan != last:
+        problems.append("makespan is not the last finish")
+    return problems
+
+
+KIND_NAMES = {0: "net_rc", 1: "cell_delay_at", 2: "slack_bwd", 3: "lse_fwd", 4: "grad_bwd"}
+
+
+def measured_kernel_costs(dev, n_levels: int, gamma: float | None = None, loss: str = "hinge",
+                          repeats: int = 5) -> dict:
+    """(kind, level) -> ms measured on the device: RUN_TIMED sequential passes
+    (one CUDA event after every launch; median of `repeats`).  The RC of all
+    levels is one streaming launch, charged to net_rc:0; launches outside the
+    graph (free pins, adjoint finish, summary) are folded into the
+    neighbouring kernel of the same stream."""
+    import statistics
+    flags = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_TIMED
+    runs = []
+    for _ in range(repeats + 1):
+        dev.run(flags, gamma=gamma, loss=loss)
+        runs.append(dev.kernel_times())
+    runs = runs[1:]                        # first run warms up
+    costs = {(k, li): 0.0 for li in range(n_levels) for k in KIND_NAMES.values()}
+    for i, (kind, level, _) in enumerate(runs[0]):
+        ms = statistics.median(r[i][2] for r in runs)
+        if kind in KIND_NAMES:
+            costs[(KIND_NAMES[kind], level)] += ms
+        elif i > 0:                        # fold "other" into the previous kernel
+            pk, pl, _ = runs[0][i - 1]
+            if pk in KIND_NAMES:
+                costs[(KIND_NAMES[pk], pl)] += ms
+    return costs
+
+
+def makespan_report(design, schedule=None, cfg: "FusionConfig | None" = None, repeats: int = 5) -> dict:
+    """The reference's makespan model (schedule_sequential / schedule_fused)
+    on MEASURED kernel costs, next to the measured sequential, two-stream and
+    fused (interleaved) passes of the same design.
+
+    Events between launches serialise the programmatic-dependent-launch
+    overlap of the untimed pass, so the raw per-launch deltas are calibrated
+    to the measured sequential pass (same proportions, same total).  The
+    model's two-lane prediction is then compared with the measured two-stream
+    pass, and the contention factor that reproduces it is fitted (the
+    reference's ``contention`` knob, fusion.py:227-249)."""
+    from .diff import _flat_of
+    import torch
+    cfg = cfg or FusionConfig()
+    flat = _flat_of(design, schedule)
+    gamma = cfg.gamma if cfg.gamma is not None else default_gamma(flat.clock_period)
+    dev = device_of(flat)
+    raw_costs = measured_kernel_costs(dev, flat.n_levels, gamma, cfg.loss, repeats)
+
+    def measure(flags):
+        ts = []
+        for i in range(repeats + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dev.run(flags, gamma=gamma, loss=cfg.loss, granularity=cfg.granularity)
+            e1.record()
+            e1.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+        return sorted(ts)[len(ts) // 2]
+
+    base = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
+    seq_ms = measure(base)
+    two_ms = measure(base | _lib.RUN_TWO_STREAM)
+    fused_ms = measure(base | _lib.RUN_FUSED)
+    total = sum(raw_costs.values()) or 1.0
+    costs = {k: v * seq_ms / total for k, v in raw_costs.items()}
+    g = build_kernel_graph(flat.n_levels, costs, cfg.granularity)
+    seq, fus = schedule_sequential(g), schedule_fused(g, 1.0)
+    lo, hi = 1.0, 8.0                       # contention reproducing the two-stream run
+    if schedule_fused(g, hi).makespan < two_ms:
+        fit = None
+    elif fus.makespan >= two_ms:
+        fit = 1.0
+    else:
+        for _ in range(50):
+            mid = 0.5 * (lo + hi)
+            lo, hi = (mid, hi) if schedule_fused(g, mid).makespan < two_ms else (lo, mid)
+        fit = 0.5 * (lo + hi)
+    return {"raw_event_sum_ms": total, "model_sequential_ms": seq.makespan,
+            "model_fused_ms": fus.makespan, "model_overlap_fraction": fus.overlap_fraction,
+            "measured_sequential_ms": seq_ms, "measured_two_stream_ms": two_ms,
+            "measured_interleaved_ms": fused_ms, "fitted_contention": fit,
+            "problems": check_schedule(g, fus) + check_schedule(g, seq)}
 
 
 @dataclass
