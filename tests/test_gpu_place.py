@@ -163,3 +163,31 @@ def test_place_c4_loop_c3():
                                             cell_of_pin=pl.cell_of_pin, cell_xy=pl.cell_xy,
                                             pin_offset=pl.pin_offset))
     dev.close()
+
+
+def test_place_c2_heavy_tail():
+    """C2 (995,808 pins, fanout up to 508; RC-tree variant off): the member
+    rounds of big nets and the chunked pass tasks under the position model."""
+    raw = G.generate_raw(G.config_c2())
+    pl = PL.synthetic_placement(raw, seed=4)
+    dev = ws.DeviceDesign(raw)
+    PL.PlacementTimer(dev, pl, loss="softplus").step()
+    check(dev, 0, raw, pl, "softplus")
+    dev.close()
+
+
+def test_place_c1_tree_persistent_pass_equivalence():
+    """The position sweep after a fused pass equals the one after a
+    sequential pass (the sweep reads only the finished pass state)."""
+    raw = G.generate_raw(G.config_c1("random_tree"))
+    pl = PL.synthetic_placement(raw, seed=8)
+    dev = ws.DeviceDesign(raw, n_corners=2)
+    for k in (0, 1):
+        dev.set_values(k, res0=pl.res0, cap0=pl.cap0, wire=pl.wire.packed(), xy=pl.xy)
+    base = _lib.RUN_WIRE | _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_POSGRAD
+    dev.run(base | _lib.RUN_FUSED, corner=0)
+    dev.run(base, corner=1)
+    for f in ("d_xy", "d_res", "d_cap", "d_slew", "d_root_cap"):
+        assert np.array_equal(dev.get(f, 0), dev.get(f, 1)), f
+    check(dev, 0, raw, pl)
+    dev.close()
