@@ -241,8 +241,9 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     import paper_2603_28381_b200 as ws
     from paper_2603_28381_b200 import placement as PL
     pl = PL.synthetic_placement(raw, seed=3)
-    dev = ws.DeviceDesign(raw, n_corners=1)
+    dev = ws.DeviceDesign(raw, n_corners=2)     # corner 1: the e2e's second input slot
     timer = PL.PlacementTimer(dev, pl)
+    PL.PlacementTimer(dev, pl, corner=1)
     stream = torch.cuda.current_stream()
     cell_xy = torch.as_tensor(pl.cell_xy, device="cuda")
     cop = torch.as_tensor(pl.cell_of_pin, device="cuda")
@@ -275,19 +276,48 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     torch.cuda.synchronize()
     dev_ms = e0.elapsed_time(e1)
     loss_last = dev.summary()
-    # e2e: positions from pinned host memory, summary back, every invocation
+    # e2e: positions from pinned host memory (copy stream, straight into one
+    # of two corner slots so invocation t+1's copy overlaps invocation t),
+    # summary back, every invocation
     rng = np.random.default_rng(seed)
     host_xy = [torch.from_numpy(np.ascontiguousarray(
         pl.xy + sigma_um * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin])).pin_memory()
         for _ in range(2)]
     h_out = torch.zeros(3, dtype=torch.float64).pin_memory()
+    xys = [dev.value_tensor("xy", b) for b in range(2)]
+    summs = [dev.tensor("summary", b) for b in range(2)]
+    cstream = torch.cuda.Stream()
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def copy_in(t):
+        b = t % 2
+        cstream.wait_event(consumed[b])
+        with torch.cuda.stream(cstream):
+            xys[b].copy_(host_xy[t % 2], non_blocking=True)
+        copied[b].record(cstream)
+
+    def e2e_inv(t, nxt=True):
+        b = t % 2
+        stream.wait_event(copied[b])
+        if nxt:
+            copy_in(t + 1)
+        dev.run(timer.flags, corner=b, gamma=timer.gamma, stream=stream)
+        consumed[b].record(stream)
+        h_out.copy_(summs[b], non_blocking=True)
+
+    for b in range(2):
+        consumed[b].record(stream)
+    copy_in(0)
+    e2e_inv(0)
+    e2e_inv(1, nxt=False)
     n_e2e = min(n_inv, 50)
     torch.cuda.synchronize()
     e0.record(stream)
+    cstream.wait_event(e0)
+    copy_in(0)
     for t in range(n_e2e):
-        xy.copy_(host_xy[t % 2], non_blocking=True)
-        dev.run(timer.flags, gamma=timer.gamma, stream=stream)
-        h_out.copy_(summ, non_blocking=True)
+        e2e_inv(t, nxt=t + 1 < n_e2e)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / n_e2e
@@ -499,14 +529,20 @@ def main():
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ke = max(3, min(args.steps, 10))
-    e0.record(stream)
-    cstream.wait_event(e0)
-    stage_copy(0)                            # the first timed step's inputs
-    for i in range(ke):
-        e2e_step(i, prefetch_next=i + 1 < ke)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_tot = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    windows = []
+    for _ in range(3):                       # median of three pipelined windows of ke steps
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0.record(stream)
+        cstream.wait_event(e0)
+        stage_copy(0)                        # the first timed step's inputs
+        for i in range(ke):
+            e2e_step(i, prefetch_next=i + 1 < ke)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        windows.append(e0.elapsed_time(e1))
+    e2e_tot = torch.tensor([sorted(windows)[1]], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / ke / world
