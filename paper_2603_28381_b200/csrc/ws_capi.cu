@@ -243,6 +243,8 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
         {
             const char* e = getenv("WS_LUT_GLOBAL");
             c.lut_global = e && e[0] == '1';
+            const char* r = getenv("WS_RC_SCHEME");
+            c.rc_cte = r && std::string(r) == "cte";
         }
         WS_CUDA(cudaStreamCreateWithFlags(&c.s_main, cudaStreamNonBlocking));
         WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamNonBlocking));

@@ -1282,6 +1282,74 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
     }
 }
 
+
+// ---- CTE-scheme RC (the paper's Algorithm 2 ablation) ---
+// A block owns CTE_NETS consecutive nets (thread = net): an exclusive scan of
+// their (members x 4) workloads in shared memory, then the block's threads
+// stride over the flattened (member, cond) tasks, each locating its net by
+// binary search in the scan.  Star-net members get their Elmore delay /
+// impulse / load there; the (net, cond) root loads use the same ordered
+// 8-partial fold as k_rc_flat.  Results are bitwise those of k_rc_flat
+// (WS_RC_SCHEME=cte selects it; RC-tree nets stay with k_rc_tree).
+constexpr int CTE_NETS = 256;
+
+__global__ void __launch_bounds__(CTE_NETS) k_rc_cte(Topo t, Corners cs)
+{
+    __shared__ int pre[CTE_NETS + 1], s0[CTE_NETS];
+    __shared__ unsigned char tree[CTE_NETS];
+    pdl_trigger();
+    const Corner& C = cs.c[blockIdx.y];
+    const int n0 = blockIdx.x * CTE_NETS, tid = threadIdx.x;
+    const int n = n0 + tid;
+    int w = 0;
+    if (n < t.N) {
+        const int a = t.net_ptr[n], b = t.net_ptr[n + 1];
+        s0[tid] = a;
+        tree[tid] = t.net_tree[n] ? 1 : 0;
+        w = tree[tid] ? 0 : (b - a) * 4;
+    }
+    pre[tid + 1] = w;
+    if (tid == 0) pre[0] = 0;
+    __syncthreads();
+    // inclusive Hillis-Steele scan over pre[1..CTE_NETS]
+    for (int off = 1; off < CTE_NETS; off <<= 1) {
+        const int v = tid >= off ? pre[tid + 1 - off] : 0;
+        __syncthreads();
+        pre[tid + 1] += v;
+        __syncthreads();
+    }
+    pdl_wait();
+    const int total = pre[CTE_NETS];
+    for (int task = tid; task < total; task += CTE_NETS) {
+        int lo = 0, hi = CTE_NETS;        // last net with pre[net] <= task
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= task) lo = mid; else hi = mid;
+        }
+        const int rel = task - pre[lo], k = rel >> 2, c = rel & 3;
+        const size_t i = (size_t)(s0[lo] + k) * 4 + c;
+        const int code = t.rc_code[s0[lo] + k];
+        const double b = C.mem_cap[i], r = C.mem_res[i];
+        const double d = __dadd_rn(0.0, __dmul_rn(r, b));
+        const double rad = __dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, r), b), d), __dmul_rn(d, d));
+        const size_t pin = (size_t)(code >> 1);
+        if (!(code & 1)) C.load[pin * 4 + c] = b;
+        C.net_delay[pin * 4 + c] = d;
+        C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+    }
+    for (int it = tid; it < CTE_NETS * 4; it += CTE_NETS) {
+        const int nl = it >> 2, c = it & 3, nn = n0 + nl;
+        if (nn >= t.N || tree[nl]) continue;
+        const int s = s0[nl], m = t.net_ptr[nn + 1] - s, root = t.net_root[nn];
+        const double l = root_load8(C.mem_cap + (size_t)s * 4 + c, 4, m);
+        C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)nn * 4 + c], l);
+        if (t.member_of_pin[root] < 0) {
+            C.net_delay[(size_t)root * 4 + c] = 0.0;
+            C.impulse[(size_t)root * 4 + c] = 0.0;
+        }
+    }
+}
+
 // tree nets (any member with a non-root parent): the whole Elmore recursion
 // per (net, cond), sequential like the reference
 __global__ void __launch_bounds__(RC_TPB) k_rc_tree(Topo t, Corners cs)
@@ -2253,7 +2321,10 @@ struct Launcher {
         if (w == 8) {
             const int nbm = (int)(((size_t)ctx.t.M * 4 + RC_TPB * RC_ITEMS - 1) / (RC_TPB * RC_ITEMS));
             const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
-            launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm);
+            if (ctx.rc_cte)
+                launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
+            else
+                launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm);
             if (ctx.any_tree) {
                 count++;
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);

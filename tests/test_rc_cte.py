@@ -1,0 +1,39 @@
+"""CTE-scheme RC kernel (the paper's Algorithm 2 ablation, WS_RC_SCHEME=cte):
+bitwise the same RC outputs and pass as the default streaming RC kernel on
+star designs (heavy tail up to 508 members) and on RC-tree designs."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_28381_b200 as ws
+from paper_2603_28381_b200 import _lib, generator as G
+
+pytestmark = pytest.mark.gpu
+FIELDS = ("load", "net_delay", "impulse", "arrival", "slew", "required", "slack", "adjoint")
+
+
+def _run(raw, scheme):
+    old = os.environ.get("WS_RC_SCHEME")
+    os.environ["WS_RC_SCHEME"] = scheme
+    try:
+        dev = ws.DeviceDesign(raw)
+    finally:
+        if old is None:
+            del os.environ["WS_RC_SCHEME"]
+        else:
+            os.environ["WS_RC_SCHEME"] = old
+    dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED)
+    out = {f: dev.get(f) for f in FIELDS}
+    dev.close()
+    return out
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c1tree", "c2"])
+def test_cte_rc_bitwise(cfg):
+    raw = G.generate_raw({"c1": G.config_c1(), "c1tree": G.config_c1("random_tree"),
+                          "c2": G.config_c2()}[cfg])
+    a, b = _run(raw, "flat"), _run(raw, "cte")
+    for f in FIELDS:
+        assert np.array_equal(a[f], b[f]), f
