@@ -114,27 +114,6 @@ struct NetSmem {
     int mptr[TASK_Q + 1];   // absolute tm_* offsets
 };
 
-// the same records from the task's blob (one round trip, k-indexed)
-__device__ __forceinline__ void load_nets_blob(const Topo& t, int k, const Task& T, NetSmem& S)
-{
-    const int i = threadIdx.x;
-    if (i <= TASK_Q) {
-        const int4 a = t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + i)];
-        const int4 b = t.fb_n[2 * ((size_t)k * (TASK_Q + 1) + i) + 1];
-        if (i <= T.nq) {
-            S.aptr[i] = b.y;
-            S.mptr[i] = b.z;
-            if (i < T.nq) {
-                S.root[i] = a.x;
-                S.flags[i] = a.y;
-                S.f0[i] = a.z;
-                S.net[i] = a.w;
-                S.e1[i] = b.x;
-            }
-        }
-    }
-}
-
 __device__ __forceinline__ void load_nets(const Topo& t, const Task& T, NetSmem& S)
 {
     const int i = threadIdx.x;
@@ -503,67 +482,7 @@ __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSme
     }
 }
 
-template <bool HARD>
-__device__ __forceinline__ void fwd_records_blob(const Topo& t, int k, const Task& T, FwdSmem& S, FwdRec& R)
-{
-    load_nets_blob(t, k, T, S.n);
-    const int c = threadIdx.x & 3, qi = threadIdx.x >> 2;
-    const size_t qs = (size_t)k * TASK_Q + qi;
-    // every load below is addressed by (task, slot) only: one round trip
-    const int4 fq = t.fb_q[qs];
-    int2 fa[FWD_NA];
-    uint4 fl[FWD_NA];
-#pragma unroll
-    for (int s = 0; s < FWD_NA; s++) {
-        fa[s] = t.fb_a[qs * FWD_NA + s];
-        if (HARD) fl[s] = t.fb_l[qs * FWD_NA + s];
-    }
-    int2 fm[ITEMS];
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) fm[s] = t.fb_m[(size_t)k * TASK_M + qi + s * TASK_Q];
-    R.nroot = fq.x;
-    R.nflags = fq.y;
-    R.a0 = fq.z;
-    R.na = fq.w;
-#pragma unroll
-    for (int s = 0; s < FWD_NA; s++) {
-        R.from[s] = fa[s].x;
-        R.arc[s] = fa[s].y;
-        if (HARD) {
-            const unsigned dw = c < 2 ? fl[s].x : fl[s].y, sw = c < 2 ? fl[s].z : fl[s].w;
-            R.dl[s] = (unsigned short)((c & 1) ? dw >> 16 : dw & 0xffff);
-            R.sl[s] = (unsigned short)((c & 1) ? sw >> 16 : sw & 0xffff);
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) {
-        R.mpin[s] = fm[s].x;
-        R.mfl[s] = fm[s].y;
-    }
-}
 
-// persistent kernel: records plus every gather that is static for the whole
-// forward sweep (RC outputs)
-template <bool HARD>
-__device__ __forceinline__ void fwd_static_gathers(const Corner& C, FwdRec& R)
-{
-    const int c = threadIdx.x & 3;
-#pragma unroll
-    for (int k = 0; k < ITEMS; k++)
-        if (R.mpin[k] >= 0) {
-            R.mnd[k] = LDG(C.net_delay + (size_t)R.mpin[k] * 4 + c);
-            if (HARD) R.mim[k] = LDG(C.impulse + (size_t)R.mpin[k] * 4 + c);
-        }
-    R.ld = (HARD && R.na > 0) ? LDG(C.load + (size_t)R.nroot * 4 + c) : 0.0;
-}
-
-template <bool HARD>
-__device__ __forceinline__ void fwd_records_static(const Topo& t, const Corner& C, int k, const Task& T,
-                                                   FwdSmem& S, FwdRec& R)
-{
-    fwd_records_blob<HARD>(t, k, T, S, R);
-    fwd_static_gathers<HARD>(C, R);
-}
 
 // arc-driven root with more than FWD_NA (but <= TASK_A) in-arcs: the same
 // arithmetic in the same order, records read in a loop
@@ -866,35 +785,6 @@ __device__ __forceinline__ void bwd_records(const Topo& t, const Task& T, BwdSme
     }
 }
 
-template <bool GRAD>
-__device__ __forceinline__ void bwd_records_blob(const Topo& t, int k, const Task& T, BwdSmem& S, BwdRec& R)
-{
-    load_nets_blob(t, k, T, S.n);
-    const bool late = (threadIdx.x & 3) >= 2;
-    const int qi = threadIdx.x >> 2;
-    int4 m1[ITEMS], m2[ITEMS];
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) {
-        const size_t ms = (size_t)k * TASK_M + qi + s * TASK_Q;
-        m1[s] = t.bb_m[2 * ms];
-        m2[s] = t.bb_m[2 * ms + 1];
-    }
-    const int4 bq = t.bb_q[(size_t)k * TASK_Q + qi];
-#pragma unroll
-    for (int s = 0; s < ITEMS; s++) {
-        R.pin[s] = m1[s].x;
-        R.fl[s] = m1[s].y;
-        R.o1t[s] = m1[s].z;
-        R.o1a[s] = m1[s].w;
-        R.e1[s] = m2[s].x;
-        R.o0[s] = m2[s].y;
-        R.no[s] = m2[s].z;
-        R.arc[s] = (GRAD && late) ? m2[s].w : -1;
-    }
-    R.nroot = bq.x;
-    R.nflags = bq.y;
-    R.ne1 = bq.z;
-}
 
 // one member (u, c): fold required over out-arcs, slack, adjoint.
 template <bool HARD, bool GRAD>
@@ -982,53 +872,7 @@ __device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int 
     return __dadd_rn(0.0, seed_term(__dsub_rn(l, C.ep_required[(size_t)e1 * 4 + 2 + j]), g, kind));
 }
 
-// persistent kernel: records plus the gathers that are static for the whole
-// backward sweep (forward outputs, endpoint seeds)
-template <bool HARD, bool GRAD>
-__device__ __forceinline__ void bwd_static_gathers(const Topo& t, const Corner& C, BwdRec& R, double g,
-                                                   int kind)
-{
-    const int c = threadIdx.x & 3, j = c - 2;
-    const bool late = c >= 2;
-#pragma unroll
-    for (int k = 0; k < ITEMS; k++) {
-        R.ado[k] = R.nd[k] = R.at[k] = R.lse[k] = R.epl[k] = R.wgt[k] = R.r0[k] = 0.0;
-        if (R.pin[k] >= 0) {
-            const int pin = R.pin[k], fl = R.fl[k];
-            if (HARD) {
-                if (R.o1a[k] >= 0) R.ado[k] = LDG(C.arc_delay + (size_t)R.o1a[k] * 4 + c);
-                R.nd[k] = LDG(C.net_delay + (size_t)pin * 4 + c);
-                R.at[k] = LDG(C.arrival + (size_t)pin * 4 + c);
-                if (!(fl & TM_ROOT))
-                    R.r0[k] = (fl & TM_MULTI_EP) ? init_required_multi(t, C, pin, c)
-                                                 : merge_req(c < 2 ? -INF : INF,
-                                                             (fl & TM_EP) ? C.ep_required[(size_t)R.e1[k] * 4 + c]
-                                                                          : (c < 2 ? -INF : INF), c);
-            }
-            if (GRAD && late && (fl & TM_EP)) {
-                R.lse[k] = LDG(C.lse_at + (size_t)pin * 2 + j);
-                R.epl[k] = C.ep_required[(size_t)R.e1[k] * 4 + 2 + j];
-            }
-        }
-        if (R.arc[k] >= 0) R.wgt[k] = LDG(C.weights + (size_t)R.arc[k] * 2 + j);
-    }
-    R.n_at = R.n_rr = R.n_seed = 0.0;
-    if (R.nroot >= 0) {
-        if (HARD) {
-            if (!(R.nflags & TQ_ROOT_MEMBER)) R.n_at = LDG(C.arrival + (size_t)R.nroot * 4 + c);
-            R.n_rr = root_init_required(t, C, R.nroot, R.nflags, R.ne1, c);
-        }
-        if (GRAD && late) R.n_seed = root_seed(t, C, R.nroot, R.nflags, R.ne1, j, g, kind);
-    }
-}
 
-template <bool HARD, bool GRAD>
-__device__ __forceinline__ void bwd_records_static(const Topo& t, const Corner& C, int k, const Task& T,
-                                                   BwdSmem& S, BwdRec& R, double g, int kind)
-{
-    bwd_records_blob<GRAD>(t, k, T, S, R);
-    bwd_static_gathers<HARD, GRAD>(t, C, R, g, kind);
-}
 
 template <bool HARD, bool GRAD, bool STATIC = false>
 __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem& S,
@@ -1982,7 +1826,7 @@ __device__ __forceinline__ void bwd_stage_issue(const Corner& C, const BwdRec& R
     cp_async_commit();
 }
 
-// bwd_static_gathers from the staged values (multi-endpoint pins, rare,
+// the backward sweep-static values from the staged copies (multi-endpoint pins, rare,
 // still fold their endpoint entries from global memory here)
 template <bool HARD, bool GRAD>
 __device__ __forceinline__ void bwd_stage_take(const Topo& t, const Corner& C, const BwdStage& st,
