@@ -225,6 +225,66 @@ def corner_batch(raw, rank, world, flags, steps, dist=None, n_total=16):
     return out
 
 
+def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5):
+    """Placement-candidate batch (north_star): 16 candidate
+    placements of C3 (cells moved by N(0, sigma) with seed 2000 + c),
+    candidate c on rank c mod N, a rank's candidates in ONE ws_run (wire RC ->
+    batched pass -> position gradients per candidate), then the candidates'
+    (TNS, WNS, loss) and dL/dxy all-gathered in candidate order (no
+    reduction: candidates are alternatives).  Device time, max over ranks."""
+    import torch
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200 import placement as PL
+    from paper_2603_28381_b200.corners import best_candidate, corners_of_rank, gather_candidates
+    mine = corners_of_rank(n_total, rank, world)
+    nc = len(mine)
+    pl = PL.synthetic_placement(raw, seed=3)
+    dev = ws.DeviceDesign(raw, n_corners=nc)
+    timers = []
+    for i, c in enumerate(mine):
+        rng = np.random.default_rng(2000 + c)
+        xy = pl.xy + sigma_um * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin]
+        timers.append(PL.PlacementTimer(dev, PL.Placement(xy, pl.res0, pl.cap0, pl.wire, pl.cell_of_pin,
+                                                          pl.cell_xy, pl.pin_offset), corner=i))
+    flags = timers[0].flags
+    stream = torch.cuda.current_stream()
+    summ = [dev.tensor("summary", i) for i in range(nc)]
+    dxy = [dev.tensor("d_xy", i) for i in range(nc)]
+
+    def step():
+        dev.run(flags, corner=0, n_corners=nc, gamma=timers[0].gamma, stream=stream)
+        s = torch.stack(summ)
+        if dist is not None:
+            return gather_candidates(s, torch.stack(dxy))
+        return s, torch.stack(dxy)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    if dist is not None:
+        dist.barrier()
+    for i in range(steps):
+        evs[i][0].record(stream)
+        s, _ = step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / steps
+    b = best_candidate(s)
+    out = {"workload": "%d placement candidates of C3 (cells moved by N(0, %.1f um)), candidate c -> "
+                       "rank c mod N, a rank's candidates in one ws_run with position gradients, "
+                       "(TNS, WNS, loss) and dL/dxy all-gathered" % (n_total, sigma_um),
+           "candidates_per_gpu": nc, "ms_per_batch": round(ms, 4),
+           "candidates_per_s": round(n_total / (ms * 1e-3), 2), "steps": steps,
+           "best": {"candidate": b, "loss": float(s[b, 2]), "tns": float(s[b, 0])}}
+    dev.close()
+    return out
+
+
 def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     """C4: the timing-driven placement loop — n_inv STA
     fwd+bwd invocations on the C3 netlist with perturbed pin coordinates,
@@ -547,9 +607,10 @@ def main():
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / ke / world
 
-    cb = None
+    cb = pb = None
     if args.corners and 16 % world == 0:
         cb = corner_batch(raw, rank, world, flags, steps=max(3, min(args.steps, 10)), dist=dist)
+        pb = candidate_batch(raw, rank, world, steps=3, dist=dist)
 
     if rank == 0:
         P, M, N, A, I, E = (dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep)
@@ -588,6 +649,8 @@ def main():
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
         if cb is not None:
             line["corner_batch"] = cb
+        if pb is not None:
+            line["candidate_batch"] = pb
         if args.placement and world == 1:
             line["placement_loop"] = placement_loop(raw, n_inv=args.placement)
         if args.cpu_baseline and world == 1:

@@ -60,3 +60,36 @@ def combine_local(summaries):
     import torch
     s = torch.stack(list(summaries))
     return torch.stack([s[:, 0].sum(), s[:, 1].min(), s[:, 2].sum()])
+
+
+def gather_candidates(summaries, d_xy=None, group=None):
+    """Placement-candidate batch (north_star: "multiple placement candidates
+    in a timing-driven placement batch"): candidates are
+    independent, so nothing is reduced — every rank's (TNS, WNS, loss) rows and
+    position gradients are gathered in candidate order.
+
+    summaries: [k, 3] fp64 tensor of this rank's k candidates; d_xy: [k, P, 2]
+    or None.  Candidate c lives on rank c mod world as its (c // world)-th
+    local candidate (corners_of_rank); returns ([world*k, 3], [world*k, P, 2])
+    in global candidate order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    k = summaries.shape[0]
+
+    def gather(t):
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t.contiguous(), group=group)
+        out = torch.stack(parts)          # out[r, i] is candidate i * world + r
+        return out.transpose(0, 1).reshape((world * k,) + tuple(t.shape[1:]))
+
+    s = gather(summaries)
+    g = gather(d_xy) if d_xy is not None else None
+    return s, g
+
+
+def best_candidate(summaries):
+    """Index of the candidate with the smallest loss (ties: lowest index)."""
+    import torch
+    loss = summaries[:, 2]
+    return int(torch.argmin(loss).item())

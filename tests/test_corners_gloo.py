@@ -87,3 +87,32 @@ def test_gloo_world2_batch_reduction(tmp_path, name):
     assert float(got["summ"][1]) == float(exp[1])                       # MIN is exact
     np.testing.assert_allclose(got["d_arc"].numpy(), sum(r[1] for r in ref).numpy(), rtol=1e-12)
     np.testing.assert_allclose(got["d_edge"].numpy(), sum(r[2] for r in ref).numpy(), rtol=1e-12)
+
+
+def _cand_worker(rank, world, port, out):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        mine = CO.corners_of_rank(6, rank, world)
+        summ = torch.stack([torch.tensor([-1.0 * c, -0.1 * c, 10.0 - c], dtype=torch.float64)
+                            for c in mine])
+        dxy = torch.stack([torch.full((5, 2), float(c), dtype=torch.float64) for c in mine])
+        s, g = CO.gather_candidates(summ, dxy)
+        if rank == 0:
+            torch.save({"s": s, "g": g, "best": CO.best_candidate(s)}, out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_candidate_gather(tmp_path):
+    """Placement candidates: rank r holds candidates r, r+2, r+4; the gather
+    returns all six in candidate order; the best is the lowest loss."""
+    out = str(tmp_path / "c.pt")
+    mp.spawn(_cand_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = torch.load(out)
+    assert got["s"][:, 0].tolist() == [-float(c) for c in range(6)]
+    assert all(float(got["g"][c, 0, 0]) == float(c) for c in range(6))
+    assert got["best"] == 5
