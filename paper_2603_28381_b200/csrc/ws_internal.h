@@ -105,6 +105,13 @@ struct PlaceCorner {
     double* sc_t = nullptr;      // (M,2) root-slew terms of the members
 };
 
+// one corner's engine + placement pointers, read by the batched sweep kernels
+// (blockIdx.y = corner)
+struct PgArgs {
+    Corner d;
+    PlaceCorner g;
+};
+
 struct CornerSlot {
     Corner d;                  // device pointers
     bool has_lse = false;      // LSE forward done since the last hard pass
@@ -138,6 +145,7 @@ struct Context {
     std::vector<int> graph_launches;  // kernels per captured graph
     PlaceTopo pt;
     std::vector<PlaceCorner> place;   // per corner once place_enable ran
+    PgArgs* pg_args = nullptr;        // device copy of {corner, place} per corner
     std::vector<cudaEvent_t> pg_events;   // [L + 2]: per backward level, fork, join
     // WS_RUN_TIMED: an event after every launch of a sequential pass, tagged
     // with the reference's kernel kind and level (fusion.py:113-160)

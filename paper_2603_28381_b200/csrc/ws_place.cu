@@ -107,12 +107,17 @@ __device__ __forceinline__ void interp_grad(const LutView& L, int lut, double qs
 
 // positions -> RC of every member edge (orc_wire); one thread per member
 __global__ void k_wire(int M, const int* __restrict__ mem_pin, const int* __restrict__ parent_pin,
-                       const double2* __restrict__ xy, const double4* __restrict__ res0,
-                       const double4* __restrict__ cap0, const double* __restrict__ wire,
-                       double4* __restrict__ res, double4* __restrict__ cap)
+                       const PgArgs* __restrict__ pa)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= M) return;
+    const PgArgs& A = pa[blockIdx.y];
+    const double2* __restrict__ xy = reinterpret_cast<const double2*>(A.g.xy);
+    const double4* __restrict__ res0 = reinterpret_cast<const double4*>(A.g.res0);
+    const double4* __restrict__ cap0 = reinterpret_cast<const double4*>(A.g.cap0);
+    const double* __restrict__ wire = A.g.wire;
+    double4* __restrict__ res = reinterpret_cast<double4*>(A.d.mem_res);
+    double4* __restrict__ cap = reinterpret_cast<double4*>(A.d.mem_cap);
     const double2 p = xy[mem_pin[k]], q = xy[parent_pin[k]];
     const double l = __dadd_rn(fabs(__dsub_rn(p.x, q.x)), fabs(__dsub_rn(p.y, q.y)));
     const double4 r0 = res0[k], c0 = cap0[k];
@@ -187,9 +192,11 @@ __device__ void pg_tree_net(const Topo& t, const Corner& C, const PlaceCorner& G
 //   A = adj + gimp (r cap - d) / imp,  d_res = A cap + gimp cap d / imp,
 //   x = A r,  y = gimp r d / imp   (d_cap = (x + gl) + y, k_pg_level)
 // (orc_posgrad_level with buf = cap).  RC-tree nets keep gimp only.
-__global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, Corner C, PlaceCorner G,
+__global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, const PgArgs* __restrict__ pa,
                                                 int u_begin, int n2)
 {
+    const Corner& C = pa[blockIdx.y].d;
+    const PlaceCorner& G = pa[blockIdx.y].g;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n2) {
         pdl_wait();
@@ -235,8 +242,10 @@ __global__ void __launch_bounds__(256) k_pg_mem(Topo t, PlaceTopo pt, Corner C, 
 }
 
 __global__ void __launch_bounds__(PG_WARPS * 32, 3) k_pg_level(Topo t, LutSrc ls, bool use_smem,
-                                                               Corner C, PlaceCorner G, int q0, int nq)
+                                                               const PgArgs* __restrict__ pa, int q0, int nq)
 {
+    const Corner& C = pa[blockIdx.y].d;
+    const PlaceCorner& G = pa[blockIdx.y].g;
     extern __shared__ __align__(16) unsigned char smem[];
     const LutView L = stage_luts(ls, C.lut_t_flat, use_smem, smem);
     const int lane = threadIdx.x & 31, grp = lane / PG_G, j = lane & 1, c = 2 + j;
@@ -365,8 +374,9 @@ __device__ __forceinline__ double sgn(double d) { return d > 0.0 ? 1.0 : (d < 0.
 // dL/dlength of member edge k and its signed x / y contributions
 // e_k = dL/dlength * sign(member - parent) (orc_pos_reduce's g * sg)
 __global__ void k_pg_len(int M, const int* __restrict__ mem_pin, const int* __restrict__ parent_pin,
-                         PlaceCorner G)
+                         const PgArgs* __restrict__ pa)
 {
+    const PlaceCorner& G = pa[blockIdx.y].g;
     pdl_wait();
     pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -387,9 +397,10 @@ __global__ void k_pg_len(int M, const int* __restrict__ mem_pin, const int* __re
 // dL/dxy of pin p: + its own edge (as a member), - the edges of its children
 // (as a parent), merged in ascending member order = orc_pos_reduce's order
 __global__ void k_pg_xy(int P, const int* __restrict__ member_of_pin, const int* __restrict__ pc_ptr,
-                        const int* __restrict__ pc_mem, const double2* __restrict__ e,
-                        double2* __restrict__ d_xy)
+                        const int* __restrict__ pc_mem, const PgArgs* __restrict__ pa)
 {
+    const double2* __restrict__ e = reinterpret_cast<const double2*>(pa[blockIdx.y].g.sc_buf);
+    double2* __restrict__ d_xy = reinterpret_cast<double2*>(pa[blockIdx.y].g.d_xy);
     pdl_wait();
     pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -520,6 +531,10 @@ void place_enable(Context& ctx)
         WS_CUDA(cudaMemset(g.gl, 0, sizeof(double) * 2 * std::max(N, 1)));
         WS_CUDA(cudaMemset(g.d_root_cap, 0, sizeof(double) * 2 * std::max(N, 1)));
     }
+    std::vector<PgArgs> pa(ctx.corners.size());
+    for (size_t ci = 0; ci < ctx.corners.size(); ci++) pa[ci] = PgArgs{ctx.corners[ci].d, ctx.place[ci]};
+    ctx.pg_args = ctx.topo_mem.alloc<PgArgs>(pa.size());
+    WS_CUDA(cudaMemcpy(ctx.pg_args, pa.data(), sizeof(PgArgs) * pa.size(), cudaMemcpyHostToDevice));
     ctx.pt.ready = true;
 }
 
@@ -527,16 +542,10 @@ int launch_wire(Context& ctx, int c0, int nc, cudaStream_t s)
 {
     const Topo& t = ctx.t;
     if (!t.M) return 0;
-    for (int k = c0; k < c0 + nc; k++) {
-        const PlaceCorner& g = ctx.place[k];
-        const Corner& d = ctx.corners[k].d;
-        k_wire<<<(t.M + 255) / 256, 256, 0, s>>>(
-            t.M, t.mem_pin, ctx.pt.parent_pin, reinterpret_cast<const double2*>(g.xy),
-            reinterpret_cast<const double4*>(g.res0), reinterpret_cast<const double4*>(g.cap0), g.wire,
-            reinterpret_cast<double4*>(d.mem_res), reinterpret_cast<double4*>(d.mem_cap));
-        WS_CHECK_LAUNCH();
-    }
-    return nc;
+    k_wire<<<dim3((t.M + 255) / 256, nc), 256, 0, s>>>(t.M, t.mem_pin, ctx.pt.parent_pin,
+                                                        ctx.pg_args + c0);
+    WS_CHECK_LAUNCH();
+    return 1;
 }
 
 int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s_pass, cudaStream_t gs,
@@ -556,48 +565,48 @@ int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s_pass, cudaStream
     // than the few located queries of a net's in-arcs
     const size_t lut_bytes = 0;
     const bool use_smem = false;
+    // arcs of lower-level targets are read before written: start from 0
     for (int k = c0; k < c0 + nc; k++) {
         const PlaceCorner& g = ctx.place[k];
-        const Corner& d = ctx.corners[k].d;
-        // arcs of lower-level targets are read before written: start from 0
         if (t.A) WS_CUDA(cudaMemsetAsync(g.gsa, 0, sizeof(double) * 2 * (size_t)t.A, s));
         if (t.P) WS_CUDA(cudaMemsetAsync(g.gsr, 0, sizeof(double) * 2 * (size_t)t.P, s));
-        bool pdl = false;        // the first sweep kernel waits for the whole pass
-        int waited = t.L;        // lowest backward level known complete
-        for (int li = t.L - 1; li >= 0; li--) {
-            const int q0 = ctx.lv_ptr_host[li], nq = ctx.lv_ptr_host[li + 1] - q0;
-            if (bwd_done && li < waited) {
-                waited = std::max(0, li - PG_GROUP + 1);
-                WS_CUDA(cudaStreamWaitEvent(s, (*bwd_done)[waited], 0));
-                pdl = false;
-            }
-            if (nq <= 0) continue;
-            const int ub = ctx.pt.tq_mptr_host[q0], un = ctx.pt.tq_mptr_host[q0 + nq] - ub;
-            if (un > 0) {
-                launch_pdl(pdl, k_pg_mem, dim3((2 * un + 255) / 256), dim3(256), 0, s, t, ctx.pt, d, g, ub,
-                           2 * un);
-                pdl = true;
-                count++;
-            }
-            launch_pdl(pdl, k_pg_level, dim3((nq + PG_WARPS * (32 / PG_G) - 1) / (PG_WARPS * (32 / PG_G))),
-                       dim3(PG_WARPS * 32), lut_bytes, s, t, ls, use_smem, d, g, q0, nq);
-            pdl = true;
-            count++;
-        }
-        if (t.M) {
-            launch_pdl(pdl, k_pg_len, dim3((t.M + 255) / 256), dim3(256), 0, s, t.M,
-                       (const int*)t.mem_pin, (const int*)ctx.pt.parent_pin, g);
-            pdl = true;
-            count++;
-        }
-        if (t.P) {
-            launch_pdl(pdl, k_pg_xy, dim3((t.P + 255) / 256), dim3(256), 0, s, t.P,
-                       (const int*)t.member_of_pin, (const int*)ctx.pt.pc_ptr, (const int*)ctx.pt.pc_mem,
-                       reinterpret_cast<const double2*>(g.sc_buf), reinterpret_cast<double2*>(g.d_xy));
-            count++;
-        }
-        WS_CHECK_LAUNCH();
     }
+    const PgArgs* pa = ctx.pg_args + c0;   // blockIdx.y = corner
+    bool pdl = false;        // the first sweep kernel waits for the whole pass
+    int waited = t.L;        // lowest backward level known complete
+    for (int li = t.L - 1; li >= 0; li--) {
+        const int q0 = ctx.lv_ptr_host[li], nq = ctx.lv_ptr_host[li + 1] - q0;
+        if (bwd_done && li < waited) {
+            waited = std::max(0, li - PG_GROUP + 1);
+            WS_CUDA(cudaStreamWaitEvent(s, (*bwd_done)[waited], 0));
+            pdl = false;
+        }
+        if (nq <= 0) continue;
+        const int ub = ctx.pt.tq_mptr_host[q0], un = ctx.pt.tq_mptr_host[q0 + nq] - ub;
+        if (un > 0) {
+            launch_pdl(pdl, k_pg_mem, dim3((2 * un + 255) / 256, nc), dim3(256), 0, s, t, ctx.pt, pa, ub,
+                       2 * un);
+            pdl = true;
+            count++;
+        }
+        launch_pdl(pdl, k_pg_level,
+                   dim3((nq + PG_WARPS * (32 / PG_G) - 1) / (PG_WARPS * (32 / PG_G)), nc),
+                   dim3(PG_WARPS * 32), lut_bytes, s, t, ls, use_smem, pa, q0, nq);
+        pdl = true;
+        count++;
+    }
+    if (t.M) {
+        launch_pdl(pdl, k_pg_len, dim3((t.M + 255) / 256, nc), dim3(256), 0, s, t.M,
+                   (const int*)t.mem_pin, (const int*)ctx.pt.parent_pin, pa);
+        pdl = true;
+        count++;
+    }
+    if (t.P) {
+        launch_pdl(pdl, k_pg_xy, dim3((t.P + 255) / 256, nc), dim3(256), 0, s, t.P,
+                   (const int*)t.member_of_pin, (const int*)ctx.pt.pc_ptr, (const int*)ctx.pt.pc_mem, pa);
+        count++;
+    }
+    WS_CHECK_LAUNCH();
     return count;
 }
 
