@@ -420,25 +420,6 @@ struct FwdRec {
     double ld, mnd[ITEMS], mim[ITEMS];
 };
 
-// numpy's np.add.reduceat segment: z_0 + pairwise_sum(z_1 .. z_{n-1})
-__device__ __forceinline__ double reduceat_sum(const double* z, int stride, int n)
-{
-    double rest = 0.0;
-    if (n - 1 >= 8 && n - 1 <= 128) {
-        double r[8];
-        for (int k = 0; k < 8; k++) r[k] = z[(1 + k) * stride];
-        int i = 8;
-        const int nn = n - 1;
-        for (; i < nn - (nn % 8); i += 8)
-            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], z[(1 + i + k) * stride]);
-        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < nn; i++) rest = __dadd_rn(rest, z[(1 + i) * stride]);
-    } else {   // numpy: sequential below 8; > 129 in-arcs: sequential (documented)
-        for (int q = 1; q < n; q++) rest = __dadd_rn(rest, z[q * stride]);
-    }
-    return __dadd_rn(z[0], rest);
-}
 
 template <bool HARD>
 __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSmem& S, FwdRec& R)
@@ -1069,19 +1050,23 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
 
 // ---- streaming RC (reduce width 8) --------------------------------------
 // The RC stage has no level dependencies, so it runs as one HBM-streaming
-// launch instead of per-task blocks: blocks [0, nbm) take RC_ITEMS
+// launch instead of per-task blocks: member blocks take RC_ITEMS
 // (member, cond) items per thread in flat member order (mem_res / mem_cap
-// read once, fully coalesced); blocks [nbm, ..) take one (net, cond) item:
-// the root load of a star net (root_cap + root_load8 over its contiguous
-// member caps), or the whole Elmore recursion of a tree net.
+// read once, fully coalesced); net blocks take one (net, cond) item: the
+// root load of a star net (root_cap + root_load8 over its contiguous member
+// caps).  Net blocks come first in the grid so the sequential folds of big
+// nets overlap the streaming member blocks (RC 116 -> 108 us at C3).
 constexpr int RC_TPB = 256, RC_ITEMS = 4;
 
-__global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
+__global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm, int nbn)
 {
     pdl_trigger();
     const Corner& C = cs.c[blockIdx.y];
-    if ((int)blockIdx.x < nbm) {
-        const size_t base = (size_t)blockIdx.x * RC_TPB * RC_ITEMS + threadIdx.x;
+    // net blocks first: the sequential root-load folds of big nets start
+    // early and overlap the streaming member blocks
+    const int bx = (int)blockIdx.x < nbn ? (int)blockIdx.x + nbm : (int)blockIdx.x - nbn;
+    if (bx < nbm) {
+        const size_t base = (size_t)bx * RC_TPB * RC_ITEMS + threadIdx.x;
         const size_t n4 = (size_t)t.M * 4;
         int code[RC_ITEMS];
 #pragma unroll
@@ -1111,7 +1096,7 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm)
         }
         return;
     }
-    const int i = ((int)blockIdx.x - nbm) * RC_TPB + threadIdx.x;
+    const int i = (bx - nbm) * RC_TPB + threadIdx.x;
     const int n = i >> 2, c = i & 3;
     if (n >= t.N) return;
     if (LDG(t.net_tree + n)) return;             // k_rc_tree
@@ -1560,11 +1545,6 @@ __device__ __forceinline__ void grid_wait(unsigned long long* ctr, unsigned long
     __syncthreads();
 }
 
-__device__ __forceinline__ void grid_sync(unsigned long long* ctr, unsigned n, unsigned long long* s_target)
-{
-    grid_arrive(ctr, n, s_target);
-    grid_wait(ctr, s_target);
-}
 
 
 // ---- per-task record blobs in shared memory (persistent kernel) ---------
@@ -2168,7 +2148,7 @@ struct Launcher {
             if (ctx.rc_cte)
                 launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
             else
-                launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm);
+                launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn);
             if (ctx.any_tree) {
                 count++;
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);
