@@ -1344,27 +1344,58 @@ struct SumArgs {
 };
 
 struct SumSmem {
-    double t[8][128], l[8][128];
+    double t[8][128], l[8][128];    // leaf phase: one warp's terms
     int last;
 };
+
+// dynamic shared memory of k_summary: the whole tree (node values and the
+// plan), when it fits (sum_tree_bytes)
+__host__ __device__ inline size_t sum_tree_bytes(int n_nodes, int n_inner, int n_heights)
+{
+    return (size_t)n_nodes * 3 * 8 + (size_t)n_inner * 2 * 4 + (size_t)(n_heights + 1) * 4;
+}
 
 // leaves strided over the warps of `ncta` blocks; the last block to finish
 // combines the tree (sync_ctr[0] counts finished blocks)
 __device__ void summary_phase(const Topo& t, const Corner& C, const SumArgs& P, double g, int kind,
-                              bool want_loss, bool want_sta, int cta, int ncta, SumSmem& S)
+                              bool want_loss, bool want_sta, int cta, int ncta, SumSmem& S,
+                              unsigned char* tree = nullptr)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* nv = C.red_tmp;   // [3 * nodes]: tns, loss, wns per node
+#ifdef WS_PROBE
+#define SSTAMP(slot)                                                                          \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && t.probe) {                                                    \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[(size_t)cta * 8 + (slot)] = _v;                                           \
+        }                                                                                     \
+    } while (0)
+#else
+#define SSTAMP(slot) do { } while (0)
+#endif
+    SSTAMP(0);
     const int nn = 2 * P.n_leaves - 1;
     for (int lf = cta * 8 + warp; lf < P.n_leaves; lf += ncta * 8) {
         const int off = P.leaf_off[lf], n = P.leaf_len[lf];
         double wmin = INF;
-        for (int k = lane; k < n; k += 32) {
-            double tt, sl, lt;
-            summary_terms(t, C, off + k, g, kind, want_loss, tt, sl, lt);
-            S.t[warp][k] = tt;
-            S.l[warp][k] = lt;
-            wmin = (sl < wmin || sl != sl) ? sl : wmin;
+        // leaves hold <= 128 terms: a lane's <= 4 terms are gathered together
+        // (one round trip), then folded in the original k order
+        double tt[4], sl[4], lt[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            tt[r] = sl[r] = lt[r] = 0.0;
+            if (lane + 32 * r < n) summary_terms(t, C, off + lane + 32 * r, g, kind, want_loss, tt[r], sl[r], lt[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int k = lane + 32 * r;
+            if (k < n) {
+                S.t[warp][k] = tt[r];
+                S.l[warp][k] = lt[r];
+                wmin = (sl[r] < wmin || sl[r] != sl[r]) ? sl[r] : wmin;
+            }
         }
         for (int o = 16; o > 0; o >>= 1) {
             const double w2 = __shfl_down_sync(WS_FULL, wmin, o);
@@ -1410,6 +1441,7 @@ __device__ void summary_phase(const Topo& t, const Corner& C, const SumArgs& P, 
         __syncwarp();
     }
     // the last block to finish combines the tree
+    SSTAMP(1);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1417,8 +1449,47 @@ __device__ void summary_phase(const Topo& t, const Corner& C, const SumArgs& P, 
         S.last = prev == (unsigned)(ncta - 1);
     }
     __syncthreads();
+    SSTAMP(2);
     if (!S.last) return;
     __threadfence();
+    if (tree) {
+        // the whole tree in shared memory: leaves and plan in one round trip,
+        // then one barrier per height instead of a global-memory round trip
+        const int ni = nn - P.n_leaves;
+        double* nd = reinterpret_cast<double*>(tree);            // [3][nn]
+        int* il = reinterpret_cast<int*>(nd + 3 * (size_t)nn);   // [ni]
+        int* ir = il + ni;                                       // [ni]
+        int* hp = ir + ni;                                       // [n_heights + 1]
+        for (int i = threadIdx.x; i < P.n_leaves; i += blockDim.x) {
+            nd[i] = LDG(nv + i);
+            nd[nn + i] = LDG(nv + nn + i);
+            nd[2 * nn + i] = LDG(nv + 2 * nn + i);
+        }
+        for (int k = threadIdx.x; k < ni; k += blockDim.x) {
+            il[k] = P.in_left[k];
+            ir[k] = P.in_right[k];
+        }
+        for (int h = threadIdx.x; h <= P.n_heights; h += blockDim.x) hp[h] = P.height_ptr[h];
+        __syncthreads();
+        for (int h = 0; h < P.n_heights; h++) {
+            for (int k = hp[h] + threadIdx.x; k < hp[h + 1]; k += blockDim.x) {
+                const int l = il[k], r = ir[k], me = P.n_leaves + k;
+                nd[me] = __dadd_rn(nd[l], nd[r]);
+                nd[nn + me] = __dadd_rn(nd[nn + l], nd[nn + r]);
+                const double a = nd[2 * nn + l], b = nd[2 * nn + r];
+                nd[2 * nn + me] = (b < a || b != b) ? b : a;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const int top = nn - 1;
+            if (want_sta) { C.summary[0] = nd[top]; C.summary[1] = nd[2 * nn + top]; }
+            if (want_loss) C.summary[2] = nd[nn + top];
+            *C.sync_ctr = 0u;
+        }
+        SSTAMP(3);
+        return;
+    }
     for (int h = 0; h < P.n_heights; h++) {
         for (int k = P.height_ptr[h] + threadIdx.x; k < P.height_ptr[h + 1]; k += blockDim.x) {
             const int l = P.in_left[k], r = P.in_right[k], me = P.n_leaves + k;
@@ -1439,12 +1510,14 @@ __device__ void summary_phase(const Topo& t, const Corner& C, const SumArgs& P, 
 }
 
 __global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, SumArgs P, double g, int kind,
-                                                 bool want_loss, bool want_sta)
+                                                 bool want_loss, bool want_sta, bool smem_tree)
 {
     __shared__ SumSmem S;
+    extern __shared__ __align__(16) unsigned char tree[];
     pdl_trigger();
     pdl_wait();
-    summary_phase(t, cs.c[blockIdx.y], P, g, kind, want_loss, want_sta, blockIdx.x, gridDim.x, S);
+    summary_phase(t, cs.c[blockIdx.y], P, g, kind, want_loss, want_sta, blockIdx.x, gridDim.x, S,
+                  smem_tree ? tree : nullptr);
 }
 
 __global__ void k_summary_empty(Corners cs, bool want_loss, bool want_sta)
@@ -2246,8 +2319,13 @@ struct Launcher {
             count++;
             return;
         }
-        launch(k_summary, dim3((pl->n_leaves + 7) / 8, nc), dim3(256), 0, s, ctx.t, cs, sum_args(),
-               g, kind, want_loss, want_sta);
+        const int nn = 2 * pl->n_leaves - 1;
+        const size_t tb = sum_tree_bytes(nn, pl->n_inner, (int)pl->height_ptr.size() - 1);
+        const bool smem_tree = tb <= 160 * 1024;
+        if (smem_tree && tb > 48 * 1024)
+            WS_CUDA(cudaFuncSetAttribute(k_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb));
+        launch(k_summary, dim3((pl->n_leaves + 7) / 8, nc), dim3(256), smem_tree ? tb : 0, s,
+               probed((pl->n_leaves + 7) / 8), cs, sum_args(), g, kind, want_loss, want_sta, smem_tree);
         count++;
     }
 };
