@@ -1058,10 +1058,17 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
 // nets overlap the streaming member blocks (RC 116 -> 108 us at C3).
 constexpr int RC_TPB = 256, RC_ITEMS = 4;
 
-__global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm, int nbn)
+__global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm, int nbn, int nbf,
+                                                    bool lse)
 {
     pdl_trigger();
     const Corner& C = cs.c[blockIdx.y];
+    if ((int)blockIdx.x >= nbn + nbm) {         // pins in no net: their initial state (k_free)
+        pdl_wait();
+        const int i = ((int)blockIdx.x - nbn - nbm) * RC_TPB + threadIdx.x;
+        if (i < t.n_free) free_pin(t, C, i, lse);
+        return;
+    }
     // net blocks first: the sequential root-load folds of big nets start
     // early and overlap the streaming member blocks
     const int bx = (int)blockIdx.x < nbn ? (int)blockIdx.x + nbm : (int)blockIdx.x - nbn;
@@ -1518,6 +1525,26 @@ __global__ void __launch_bounds__(256) k_summary(Topo t, Corners cs, SumArgs P, 
     pdl_wait();
     summary_phase(t, cs.c[blockIdx.y], P, g, kind, want_loss, want_sta, blockIdx.x, gridDim.x, S,
                   smem_tree ? tree : nullptr);
+}
+
+// the adjoints finished after the level loop (k_fin) and the summary
+// (k_summary) are independent: one launch, fin blocks first
+__global__ void __launch_bounds__(256) k_fin_summary(Topo t, Corners cs, SumArgs P, double g, int kind,
+                                                     bool want_loss, bool want_sta, bool smem_tree,
+                                                     int nb_fin)
+{
+    __shared__ SumSmem S;
+    extern __shared__ __align__(16) unsigned char tree[];
+    pdl_trigger();
+    pdl_wait();
+    const Corner& C = cs.c[blockIdx.y];
+    if ((int)blockIdx.x < nb_fin) {
+        const int i = blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < 2 * t.n_fin) fin_item(t, C, i, g, kind);
+        return;
+    }
+    summary_phase(t, C, P, g, kind, want_loss, want_sta, (int)blockIdx.x - nb_fin, (int)gridDim.x - nb_fin,
+                  S, smem_tree ? tree : nullptr);
 }
 
 __global__ void k_summary_empty(Corners cs, bool want_loss, bool want_sta)
@@ -2212,16 +2239,21 @@ struct Launcher {
         launch(k_free, grid1(ctx.t.n_free, 256), dim3(256), 0, s, ctx.t, cs, lse);
         count++;
     }
-    void rc(cudaStream_t s, int w)
+    // with_free (streaming RC only): the free pins' initial state rides in
+    // the same launch (returns true when it did)
+    bool rc(cudaStream_t s, int w, bool with_free = false, bool lse = false)
     {
-        if (!ctx.t.n_tasks) return;
+        if (!ctx.t.n_tasks) return false;
+        bool took_free = false;
         if (w == 8) {
             const int nbm = (int)(((size_t)ctx.t.M * 4 + RC_TPB * RC_ITEMS - 1) / (RC_TPB * RC_ITEMS));
             const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
+            const int nbf = (with_free && !ctx.rc_cte) ? (ctx.t.n_free + RC_TPB - 1) / RC_TPB : 0;
+            took_free = with_free && !ctx.rc_cte;
             if (ctx.rc_cte)
                 launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
             else
-                launch(k_rc_flat, dim3(nbm + nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn);
+                launch(k_rc_flat, dim3(nbm + nbn + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn, nbf, lse);
             if (ctx.any_tree) {
                 count++;
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);
@@ -2230,6 +2262,7 @@ struct Launcher {
             launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
         }
         count++;
+        return took_free;
     }
     // WS_PROBE builds: launch i stamps into probe + i * PROBE_STRIDE
     static constexpr size_t PROBE_STRIDE = 8 * 2048;
@@ -2262,6 +2295,25 @@ struct Launcher {
     {
         if (!ctx.t.n_fin) return;
         launch(k_fin, grid1(2 * ctx.t.n_fin, 256), dim3(256), 0, s, ctx.t, cs, g, kind);
+        count++;
+    }
+    // fin + summary as one launch (fused pass)
+    void fin_summary(cudaStream_t s, double g, int kind)
+    {
+        const SumPlan* pl = ctx.tns_plan;
+        if (pl->n == 0) {
+            fin(s, g, kind);
+            summary(s, g, kind, true, true);
+            return;
+        }
+        const int nb_fin = ctx.t.n_fin ? (2 * ctx.t.n_fin + 255) / 256 : 0;
+        const int nn = 2 * pl->n_leaves - 1;
+        const size_t tb = sum_tree_bytes(nn, pl->n_inner, (int)pl->height_ptr.size() - 1);
+        const bool smem_tree = tb <= 160 * 1024;
+        if (smem_tree && tb > 48 * 1024)
+            WS_CUDA(cudaFuncSetAttribute(k_fin_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb));
+        launch(k_fin_summary, dim3(nb_fin + (pl->n_leaves + 7) / 8, nc), dim3(256), smem_tree ? tb : 0, s,
+               ctx.t, cs, sum_args(), g, kind, true, true, smem_tree, nb_fin);
         count++;
     }
     void slack_all(cudaStream_t s)
@@ -2350,15 +2402,13 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         if (lse) la.persistent<true, true>(s, w, g, kind);
         else la.persistent<false, false>(s, w, g, kind);
     } else if (fused) {
-        la.free_pins(s, true);
-        la.rc(s, w);
+        if (!la.rc(s, w, true, true)) la.free_pins(s, true);
         for (int li = 0; li < L; li++) la.fwd<true, true>(s, li, g);
         for (int li = L - 1; li >= 0; li--) {
             la.bwd<true, true>(s, li, g, kind);
             if (bwd_done) WS_CUDA(cudaEventRecord((*bwd_done)[li], s));
         }
-        la.fin(s, g, kind);
-        la.summary(s, g, kind, true, true);
+        la.fin_summary(s, g, kind);
     } else if (two) {
         // stream S: the hard pass; stream G: LSE + gradients, gated per
         // granularity-g level group on S's forward (fusion.py:151-157)
