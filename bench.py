@@ -607,6 +607,48 @@ def main():
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / ke / world
 
+    # per-kernel-class breakdown of the same pass: a fused pass with a CUDA
+    # event after every launch (the events serialise the PDL overlap, so the
+    # classes sum to more than the pass), and the ncu-measured DRAM bytes of
+    # each class (profiles/traffic_*.json) over its event time
+    kclass = None
+    if rank == 0:
+        tflags = (flags & ~_lib.RUN_GRAPH) | _lib.RUN_TIMED
+        runs = []
+        for _ in range(4):
+            dev.run(tflags, stream=stream)
+            runs.append(dev.kernel_times())
+        names = {0: "k_rc_flat (+free pins)", 1: "k_fwd<1,1> (fwd+LSE level)",
+                 2: "k_bwd<1,1> (bwd+grad level)", 5: "k_fin_summary"}
+        acc = {}
+        for kt in runs[1:]:
+            for kind, lvl, ms in kt:
+                a = acc.setdefault(kind, [0, 0.0])
+                a[0] += 1
+                a[1] += ms
+        traffic_pk = {}
+        tp = os.path.join(REPO, "profiles", "traffic_r01.json")
+        if os.path.exists(tp):
+            try:
+                for k, v in json.load(open(tp)).get("per_kernel", {}).items():
+                    for key, nm in (("k_rc_flat", 0), ("k_fwd<", 1), ("k_bwd<", 2), ("k_fin_summary", 5)):
+                        if key in k:
+                            traffic_pk[nm] = v["dram_bytes"] / max(1, v["launches"])
+            except Exception:
+                traffic_pk = {}
+        kclass = []
+        for kind in (1, 2, 0, 5):
+            if kind not in acc:
+                continue
+            n, tot = acc[kind]
+            avg_us = 1e3 * tot / n
+            row = {"kernel": names[kind], "launches_per_pass": n // (len(runs) - 1),
+                   "avg_launch_us": round(avg_us, 2)}
+            if kind in traffic_pk:
+                row["dram_bytes_per_launch"] = int(traffic_pk[kind])
+                row["dram_gbs"] = round(traffic_pk[kind] / (avg_us * 1e-6) / 1e9, 1)
+            kclass.append(row)
+
     cb = pb = None
     if args.corners and 16 % world == 0:
         cb = corner_batch(raw, rank, world, flags, steps=max(3, min(args.steps, 10)), dist=dist)
@@ -647,6 +689,8 @@ def main():
                 "clocks": clk.summary(),
                 "result": {"tns": tns, "wns": wns, "loss": loss},
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
+        if kclass:
+            line["roofline"]["kernel_classes"] = kclass
         if cb is not None:
             line["corner_batch"] = cb
         if pb is not None:

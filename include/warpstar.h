@@ -129,8 +129,8 @@ enum ws_run_flags {
     WS_RUN_WIRE = 512u,      /* first: mem_res / mem_cap from the positions (WS_V_XY ...) */
     WS_RUN_POSGRAD = 1024u,  /* last (needs HARD|LSE|GRAD in the same call): slew / load
                                 adjoint sweep, Elmore adjoint, dL/dxy */
-    WS_RUN_TIMED = 2048u     /* sequential mode only: a CUDA event after every launch, read
-                                back with ws_kernel_times (measured KernelGraph costs) */
+    WS_RUN_TIMED = 2048u     /* sequential or fused mode, no graph: a CUDA event after every
+                                launch, read back with ws_kernel_times (measured costs) */
 };
 
 enum ws_loss_kind { WS_LOSS_HINGE = 0, WS_LOSS_SOFTPLUS = 1 };

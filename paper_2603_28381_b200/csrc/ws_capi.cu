@@ -376,9 +376,9 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
         const unsigned need = WS_RUN_HARD | WS_RUN_LSE | WS_RUN_GRAD;
         if ((flags & WS_RUN_POSGRAD) && (flags & need) != need)
             throw ws::Error(WS_ERR_STATE, "WS_RUN_POSGRAD needs HARD|LSE|GRAD in the same run");
-        if ((flags & WS_RUN_TIMED) &&
-            (flags & (WS_RUN_FUSED | WS_RUN_TWO_STREAM | WS_RUN_PERSISTENT | WS_RUN_GRAPH)))
-            throw ws::Error(WS_ERR_VALUE, "WS_RUN_TIMED needs the sequential mode without graph capture");
+        if ((flags & WS_RUN_TIMED) && (flags & (WS_RUN_TWO_STREAM | WS_RUN_PERSISTENT | WS_RUN_GRAPH)))
+            throw ws::Error(WS_ERR_VALUE,
+                            "WS_RUN_TIMED needs the sequential or fused mode without graph capture");
         if ((flags & WS_RUN_POSGRAD) && (flags & WS_RUN_PERSISTENT))
             throw ws::Error(WS_ERR_VALUE, "WS_RUN_POSGRAD is not available with WS_RUN_PERSISTENT");
         if (flags & (WS_RUN_WIRE | WS_RUN_POSGRAD)) ws::place_enable(c);

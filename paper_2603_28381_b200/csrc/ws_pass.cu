@@ -2402,13 +2402,23 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         if (lse) la.persistent<true, true>(s, w, g, kind);
         else la.persistent<false, false>(s, w, g, kind);
     } else if (fused) {
+        // WS_RUN_TIMED: kinds 0 RC, 1 fused forward+LSE level, 2 fused
+        // backward+gradient level, 5 tail (the events serialise the PDL overlap)
+        la.timed = flags & WS_RUN_TIMED;
+        la.mark(s, 5, -1);
         if (!la.rc(s, w, true, true)) la.free_pins(s, true);
-        for (int li = 0; li < L; li++) la.fwd<true, true>(s, li, g);
+        la.mark(s, 0, 0);
+        for (int li = 0; li < L; li++) {
+            la.fwd<true, true>(s, li, g);
+            la.mark(s, 1, li);
+        }
         for (int li = L - 1; li >= 0; li--) {
             la.bwd<true, true>(s, li, g, kind);
             if (bwd_done) WS_CUDA(cudaEventRecord((*bwd_done)[li], s));
+            la.mark(s, 2, li);
         }
         la.fin_summary(s, g, kind);
+        la.mark(s, 5, -1);
     } else if (two) {
         // stream S: the hard pass; stream G: LSE + gradients, gated per
         // granularity-g level group on S's forward (fusion.py:151-157)
