@@ -168,3 +168,35 @@ class PlacementTimer:
         """Host copies of every position-gradient array of the last step."""
         return {k: self.dev.get(k, self.corner)
                 for k in ("d_res", "d_cap", "d_root_cap", "d_slew", "d_len", "d_xy")}
+
+
+def descend(timer: PlacementTimer, placement: Placement, steps: int = 20, step_um: float = 1.0,
+            stream=None):
+    """A timing-driven placement loop on the device: every iteration runs one
+    PlacementTimer step (wire RC -> pass -> dL/dxy), reduces the pin
+    gradients to their cells and moves every cell against its gradient by at
+    most ``step_um`` (the gradient is normalised by its largest cell
+    component, so the step is scale-free).  Returns the (loss, tns, wns)
+    history; the final coordinates stay in the timer's corner.
+
+    This is the C4 workload with real gradient steps instead of random
+    perturbations."""
+    import torch
+    dev = timer.dev
+    xy = torch.as_tensor(placement.xy, device="cuda").clone()
+    cell_xy = torch.as_tensor(placement.cell_xy, device="cuda").clone()
+    cop = torch.as_tensor(placement.cell_of_pin, device="cuda")
+    off = torch.as_tensor(placement.pin_offset, device="cuda")
+    n_cells = cell_xy.shape[0]
+    hist = []
+    for _ in range(steps):
+        torch.add(cell_xy.index_select(0, cop), off, out=xy)
+        tns, wns, loss = timer.step(xy, stream=stream)
+        hist.append((loss, tns, wns))
+        g = cell_gradients(timer.grad_xy_tensor(), cop, n_cells)
+        scale = g.abs().max()
+        if float(scale) == 0.0:
+            break
+        cell_xy -= (step_um / scale) * g
+    dev.sync(stream)
+    return hist

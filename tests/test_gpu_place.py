@@ -191,3 +191,17 @@ def test_place_c1_tree_persistent_pass_equivalence():
         assert np.array_equal(dev.get(f, 0), dev.get(f, 1)), f
     check(dev, 0, raw, pl)
     dev.close()
+
+
+def test_descend_reduces_the_timing_loss():
+    """Gradient steps on cell positions (dL/dxy reduced to cells) lower the
+    hinge-TNS loss of a C1 design."""
+    raw = G.generate_raw(G.config_c1())
+    pl = PL.synthetic_placement(raw, seed=5)
+    dev = ws.DeviceDesign(raw)
+    timer = PL.PlacementTimer(dev, pl)
+    hist = PL.descend(timer, pl, steps=15, step_um=2.0)
+    losses = [h[0] for h in hist]
+    assert losses[-1] < losses[0]
+    assert min(losses[1:]) < losses[0]
+    dev.close()
