@@ -285,6 +285,44 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
     return out
 
 
+def c2_sta(steps=20):
+    """C2: the ICCAD-2015-shaped 995,808-pin heavy-tail
+    netlist, forward AT / RAT / slack + TNS/WNS only (run_engine), one B200;
+    CUDA events per pass, a >L2 buffer rewritten between passes.  Roofline
+    on B_sta."""
+    import torch
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200 import _lib, generator as G
+    raw = G.generate_raw(G.config_c2())
+    dev = ws.DeviceDesign(raw)
+    flags = _lib.RUN_HARD | _lib.RUN_GRAPH
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        dev.run(flags, stream=stream)
+    ts = []
+    for i in range(steps):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dev.run(flags, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    P, M, N, A, I, E = dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep
+    B = 224 * P + 76 * M + 44 * N + 76 * A + 68 * I + 36 * E
+    peak, _ = measured_peaks()
+    tns, wns, _ = dev.summary()
+    out = {"workload": "C2 ICCAD-2015-shaped 995,808-pin heavy-tail netlist: forward AT/RAT/slack + "
+                       "TNS/WNS (run_engine)", "pins": P, "levels": dev.n_levels,
+           "ms_per_pass": round(ms, 4), "algorithmic_bytes": B,
+           "achieved_gbs": round(B / (ms * 1e-3) / 1e9, 1), "frac": round(B / (ms * 1e-3) / 1e9 / peak, 4),
+           "launches": dev.last_launch_count(), "tns": tns, "wns": wns}
+    dev.close()
+    return out
+
+
 def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     """C4: the timing-driven placement loop — n_inv STA
     fwd+bwd invocations on the C3 netlist with perturbed pin coordinates,
@@ -697,6 +735,8 @@ def main():
             line["candidate_batch"] = pb
         if args.placement and world == 1:
             line["placement_loop"] = placement_loop(raw, n_inv=args.placement)
+        if args.corners and world == 1:
+            line["c2_sta"] = c2_sta()
         if args.cpu_baseline and world == 1:
             r = time_reference(raw, max_passes=3, budget_s=25.0)
             line["cpu_baseline"] = {"value": round(r["ms"], 3), "unit": "ms", "cores": 1,
