@@ -258,7 +258,7 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
             return gather_candidates(s, torch.stack(dxy))
         return s, torch.stack(dxy)
 
-    for _ in range(2):
+    for _ in range(5):                       # first calls in a process are slower
         step()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -690,7 +690,7 @@ def main():
     cb = pb = None
     if args.corners and 16 % world == 0:
         cb = corner_batch(raw, rank, world, flags, steps=max(3, min(args.steps, 10)), dist=dist)
-        pb = candidate_batch(raw, rank, world, steps=3, dist=dist)
+        pb = candidate_batch(raw, rank, world, steps=6, dist=dist)
 
     if rank == 0:
         P, M, N, A, I, E = (dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep)
