@@ -128,3 +128,19 @@ def test_wire_model_identity_and_lengths():
     # calibration keeps the mean RC of the generated design
     assert np.allclose(res.mean(axis=0), np.asarray(raw.mem_res).mean(axis=0), rtol=1e-12)
     assert np.allclose(cap.mean(axis=0), np.asarray(raw.mem_cap).mean(axis=0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["kat_chain6", "kat_diamond", "kat_two_input", "kat_tie_break",
+                                  "kat_flat_nets", "gen_tree_1200", "gen_heavy_1500",
+                                  "gen_single_in", "gen_uniform_tree"])
+def test_position_gradient_fd_golden_designs(name):
+    """FD pinning on the reference's own test designs (the golden fixtures'
+    netlists, softplus loss so every endpoint contributes)."""
+    raw = raw_of(load(name))
+    pl, flat, gamma, res, cap, gr, pg = _setup(raw, "softplus")
+    g = pg.d_xy.ravel()
+    if not np.abs(g).max() > 0:
+        pytest.skip("no position sensitivity in this design")
+    for fi in np.argsort(-np.abs(g))[:4]:
+        fd = _fd_xy(pl, flat, gamma, "softplus", fi, 1e-3)
+        assert abs(fd - g[fi]) <= 1e-5 * abs(g[fi]), (name, fi, fd, g[fi])
