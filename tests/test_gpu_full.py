@@ -131,3 +131,42 @@ def test_placement_perturbation_parity():
         for f in G_FIELDS:
             assert grad_close(dev.get(f, 1), getattr(og, f)), (t, f)
     dev.close()
+
+
+@pytest.mark.parametrize("cfg_name", ["c1tree", "c2"])
+def test_softplus_loss_full_size(cfg_name):
+    """Softplus endpoint loss (diff.py:192-212: max(v,0) + g log1p(exp(-|v|/g)),
+    seed sigmoid(v/g)) at full size, custom gamma, all modes."""
+    raw, ofl = setup(cfg_name)
+    dev = ws.DeviceDesign(raw)
+    ost = O.run_engine(ofl)
+    gamma = 0.02 * ofl.clock_period
+    og = O.timing_gradients(ofl, ost, gamma=gamma, loss="softplus")
+    ref = None
+    for extra in (_lib.RUN_FUSED, _lib.RUN_TWO_STREAM, _lib.RUN_PERSISTENT, 0):
+        dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | extra, gamma=gamma, loss="softplus")
+        got = {f: dev.get(f) for f in G_FIELDS}
+        for f in G_FIELDS:
+            assert grad_close(got[f], getattr(og, f)), (extra, f)
+        assert dev.summary()[2] == pytest.approx(og.loss, rel=1e-9)
+        if ref is None:
+            ref = got
+        else:
+            for f in G_FIELDS:
+                assert np.array_equal(got[f], ref[f]), (extra, f)
+    dev.close()
+
+
+@pytest.mark.parametrize("gran", [1, 7, 60])
+def test_two_stream_granularity_bitwise(gran):
+    """fusion.py:151-157 event granularity g: the two-stream pass equals the
+    fused pass bitwise for any g (only the overlap changes)."""
+    raw, ofl = setup("c1")
+    dev = ws.DeviceDesign(raw)
+    base = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
+    dev.run(base | _lib.RUN_FUSED)
+    ref = {f: dev.get(f) for f in ST_FIELDS + G_FIELDS}
+    dev.run(base | _lib.RUN_TWO_STREAM, granularity=gran)
+    for f in ST_FIELDS + G_FIELDS:
+        assert np.array_equal(dev.get(f), ref[f]), (gran, f)
+    dev.close()
