@@ -62,7 +62,7 @@ def combine_local(summaries):
     return torch.stack([s[:, 0].sum(), s[:, 1].min(), s[:, 2].sum()])
 
 
-def gather_candidates(summaries, d_xy=None, group=None):
+def gather_candidates(summaries, d_xy=None, group=None, n_candidates=None):
     """Placement-candidate batch (north_star: "multiple placement candidates
     in a timing-driven placement batch"): candidates are
     independent, so nothing is reduced — every rank's (TNS, WNS, loss) rows and
@@ -70,18 +70,33 @@ def gather_candidates(summaries, d_xy=None, group=None):
 
     summaries: [k, 3] fp64 tensor of this rank's k candidates; d_xy: [k, P, 2]
     or None.  Candidate c lives on rank c mod world as its (c // world)-th
-    local candidate (corners_of_rank); returns ([world*k, 3], [world*k, P, 2])
-    in global candidate order."""
+    local candidate (corners_of_rank); returns ([n, 3], [n, P, 2]) in global
+    candidate order.  ``n_candidates`` (default world*k) may leave the ranks
+    with unequal counts (n % world != 0): every rank then pads to
+    ceil(n/world) rows so the all_gather shapes agree, and the padding is
+    dropped after the reorder."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     k = summaries.shape[0]
+    if n_candidates is None:
+        n_candidates = world * k
+    kmax = -(-n_candidates // world)           # ceil: every rank sends kmax rows
+    if k != len(corners_of_rank(n_candidates, rank, world)):
+        raise ValueError(f"rank {rank} holds {k} candidates, expected "
+                         f"{len(corners_of_rank(n_candidates, rank, world))} of {n_candidates}")
 
     def gather(t):
+        t = t.contiguous()
+        if k < kmax:                            # uneven split: pad to a common shape
+            pad = torch.zeros((kmax - k,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            t = torch.cat([t, pad])
         parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t.contiguous(), group=group)
+        dist.all_gather(parts, t, group=group)
         out = torch.stack(parts)          # out[r, i] is candidate i * world + r
-        return out.transpose(0, 1).reshape((world * k,) + tuple(t.shape[1:]))
+        out = out.transpose(0, 1).reshape((world * kmax,) + tuple(t.shape[1:]))
+        return out[:n_candidates]         # padding rows sort last; drop them
 
     s = gather(summaries)
     g = gather(d_xy) if d_xy is not None else None

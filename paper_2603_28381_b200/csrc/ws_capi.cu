@@ -246,8 +246,11 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
             const char* r = getenv("WS_RC_SCHEME");
             c.rc_cte = r && std::string(r) == "cte";
         }
-        WS_CUDA(cudaStreamCreateWithFlags(&c.s_main, cudaStreamNonBlocking));
-        WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamNonBlocking));
+        // blocking streams: with a NULL stream argument the context's work is
+        // ordered after (and before) work on the legacy default stream, the
+        // stream a caller that never chose one (torch's default) writes on
+        WS_CUDA(cudaStreamCreateWithFlags(&c.s_main, cudaStreamDefault));
+        WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamDefault));
         ws::build_topology(c, d);
         ws::summary_plan_init(c);
         c.corners.resize(n_corners);

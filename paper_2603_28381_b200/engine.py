@@ -25,18 +25,27 @@ from .netlist import RawDesign
 _LATE = slice(2, 4)
 
 
+_CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: torch's default stream has handle 0
+
+
 def _stream_handle(stream):
+    """The cudaStream_t the engine enqueues on: the caller's torch stream.
+    Torch's default stream reports handle 0, which the C ABI would read as
+    "the context's own stream"; it is passed as cudaStreamLegacy instead so
+    the engine's copies and kernels stay ordered with the caller's torch work
+    (a default-stream ``torch.add`` followed by ``set_values``)."""
     if stream is None:
         try:
             import torch
             if torch.cuda.is_available():
-                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+                h = torch.cuda.current_stream().cuda_stream
+                return ctypes.c_void_p(h or _CUDA_STREAM_LEGACY)
         except Exception:  # torch absent / no device: the library's own stream
             pass
         return ctypes.c_void_p(0)
     if isinstance(stream, int):
-        return ctypes.c_void_p(stream)
-    return ctypes.c_void_p(stream.cuda_stream)
+        return ctypes.c_void_p(stream or _CUDA_STREAM_LEGACY)
+    return ctypes.c_void_p(stream.cuda_stream or _CUDA_STREAM_LEGACY)
 
 
 class _CudaArray:
@@ -129,20 +138,25 @@ class DeviceDesign:
             if hasattr(a, "is_cuda"):
                 # torch tensor: device memory (D2D) or (pinned) host memory (async H2D)
                 import torch
+                src = a
                 a = a.contiguous()
                 if a.dtype != torch.float64:
                     raise TypeError(f"{name}: expected float64")
                 p, on_dev = ctypes.c_void_p(a.data_ptr()), 1 if a.is_cuda else 0
                 keep = a
+                temp_host = (not a.is_cuda) and a is not src
             else:
                 keep = np.ascontiguousarray(a, dtype=np.float64)
                 p = ptr(keep)
+                temp_host = False   # pageable H2D: staged before the call returns
             n = ctypes.c_int64()
             dp = ctypes.c_void_p()
             check(L.ws_value_ptr(self._h, corner, f, ctypes.byref(dp), ctypes.byref(n)))
             if (keep.numel() if hasattr(keep, "numel") else keep.size) != n.value:
                 raise ValueError(f"{name}: expected {n.value} values")
             check(L.ws_set_values(self._h, corner, f, p, on_dev, _stream_handle(stream)))
+            if temp_host:   # a contiguous copy of a pinned tensor: let the DMA land first
+                self.sync(stream)
             del keep
 
     def perturb(self, corner: int, base_corner: int, seed: int, sigma: float = 0.01, stream=None):

@@ -184,6 +184,15 @@ class RawDesign:
     def normalized(self) -> "RawDesign":
         """Contiguous arrays with the dtypes the C-ABI expects."""
         def i32(a, shape=None):
+            a = np.asarray(a)
+            if a.dtype != _I32 and a.size:
+                if not np.issubdtype(a.dtype, np.integer):
+                    if not np.array_equal(a, np.trunc(a)):
+                        raise ValueError("index arrays must hold integers")
+                lo, hi = a.min(), a.max()
+                if lo < np.iinfo(_I32).min or hi > np.iinfo(_I32).max:
+                    raise ValueError(f"index {hi if hi > 0 else lo} does not fit the device's "
+                                     f"int32 indices (ADVICE r1: no silent wrap-around)")
             a = np.ascontiguousarray(a, dtype=_I32)
             return a.reshape(shape) if shape is not None else a
 

@@ -180,6 +180,107 @@ def edge_kinds_design():
     return checked(Design(names, cells, nets, pis, eps, T))
 
 
+def multi_out_design():
+    """Pins with more than one out-arc: a two-output cell
+    whose input pins each drive 2 arcs, a free primary input (in no net)
+    driving arcs into two cells, a feedthrough root that also sources arcs
+    into two cells at different levels, a member whose two out-arcs land in
+    nets of different levels, a 4-in-arc root (past the register fast path)
+    and an endpoint member that also drives arcs."""
+    rng = np.random.default_rng(11)
+    s_ax = np.array([1e-12, 1.5e-11, 6e-11, 2e-10])
+    l_ax = np.array([1e-15, 8e-15, 1e-13])
+
+    def lut(scale):
+        return Lut2D(s_ax, l_ax, scale * (1e-11 + rng.uniform(0.5, 1.5, (4, 3)) * 1e-11))
+
+    def arc(f, t):
+        return TimingArc(f, t, [lut(1.0), lut(1.1), lut(1.0), lut(1.2)],
+                         [lut(0.5), lut(0.6), lut(0.5), lut(0.7)])
+
+    names = ["pi0", "pi1", "x", "y", "z", "a.o1", "a.o2", "f", "g", "h", "k", "l", "b.out",
+             "m", "n", "c.out", "d.out", "po1", "po2", "po3"]
+    P = {nm: i for i, nm in enumerate(names)}
+    res = lambda m: rng.uniform(100, 2000, (m, 4))
+    cap = lambda m: rng.uniform(0.5e-15, 5e-15, (m, 4))
+    rc = lambda: rng.uniform(1e-15, 3e-15, 4)
+
+    def net(root, members, parents):
+        m = len(members)
+        return Net(P[root], [P[x] for x in members], [P[x] for x in parents], res(m), cap(m), rc())
+
+    nets = [
+        net("pi1", ["x", "y", "z"], ["pi1", "x", "pi1"]),         # PI-rooted tree net
+        net("a.o1", ["f", "g"], ["a.o1", "a.o1"]),
+        net("a.o2", ["h"], ["a.o2"]),
+        net("f", ["k", "l"], ["f", "k"]),                          # feedthrough root (f in a.o1's net)
+        net("b.out", ["m", "n"], ["b.out", "b.out"]),
+        net("c.out", ["po1"], ["c.out"]),
+        net("d.out", ["po2", "po3"], ["d.out", "po2"]),
+    ]
+    A = lambda f, t: arc(P[f], P[t])
+    cells = [
+        # two-output cell: x and pi0 -> a.o1, x and y -> a.o2
+        Cell([A("x", "a.o1"), A("pi0", "a.o1"), A("x", "a.o2"), A("y", "a.o2")]),
+        # 4 in-arcs, one from the free PI
+        Cell([A("pi0", "b.out"), A("g", "b.out"), A("h", "b.out"), A("z", "b.out")]),
+        Cell([A("f", "c.out"), A("k", "c.out"), A("m", "c.out")]),
+        Cell([A("l", "d.out"), A("f", "d.out"), A("n", "d.out"), A("y", "d.out"), A("g", "d.out")]),
+    ]
+    T = 9e-11
+    pis = [PrimaryInput(P["pi0"], [1e-12, 2e-12, 3e-12, 4e-12], 2e-12),
+           PrimaryInput(P["pi1"], [2e-12, 2e-12, 5e-12, 6e-12], 3e-12)]
+    eps = [Endpoint(P["po1"], [0, 0, 0.6 * T, 0.7 * T]), Endpoint(P["po2"], [0, 0, T, T]),
+           Endpoint(P["po3"], [0, 0, 0.5 * T, T]), Endpoint(P["g"], [0, 0, 0.2 * T, 0.3 * T]),
+           Endpoint(P["po3"], [1e-12, 0, 0.4 * T, 0.9 * T])]
+    return checked(Design(names, cells, nets, pis, eps, T))
+
+
+def add_multi_out_arcs(design, seed, frac=0.15, wide=(140,), loops=(4, 5, 6, 9, 12, 17)):
+    """Mutate a generated design so that many pins drive several arcs: a
+    fraction `frac` of the member pins gains an extra arc into the root of a
+    net at a strictly higher level (added to the cell that already drives
+    that root, so every target keeps a single driving cell; edges that go up
+    in level cannot close a cycle).  Roots listed in `wide` / `loops` get that
+    many extra in-arcs (the > 128 wide-net task and the > 3 in-arc loop)."""
+    rng = np.random.default_rng(seed)
+    flat = flatten(design)
+    level_of = flat.schedule.level_of
+    mem_net = {int(p): int(n) for p, n in zip(flat.mem_pin, flat.mem_net)}
+    cell_of_root = {}
+    for ci, cell in enumerate(design.cells):
+        for a in cell.arcs:
+            cell_of_root[a.to_pin] = ci
+    roots = [(int(r), int(level_of[n])) for n, r in enumerate(flat.net_root)
+             if int(r) in cell_of_root]
+    roots.sort(key=lambda x: x[1])
+    root_lv = np.array([lv for _, lv in roots])
+    members = sorted(mem_net)
+
+    def add(u, r):
+        ci = cell_of_root[r]
+        tmpl = design.cells[ci].arcs[0]
+        design.cells[ci].arcs.append(TimingArc(u, r, list(tmpl.delay_luts), list(tmpl.slew_luts)))
+
+    def targets_above(lv):
+        i = int(np.searchsorted(root_lv, lv, side="right"))
+        return roots[i:]
+
+    for u in members:
+        if rng.random() >= frac:
+            continue
+        up = targets_above(level_of[mem_net[u]])
+        if up:
+            add(u, up[int(rng.integers(len(up)))][0])
+    top = roots[len(roots) // 2:]
+    for k in list(wide) + list(loops):
+        r, lv = top[int(rng.integers(len(top)))]
+        cand = [u for u in members if level_of[mem_net[u]] < lv]
+        for u in rng.choice(cand, size=min(k, len(cand)), replace=False):
+            add(int(u), r)
+    return checked(design)
+
+
 def cases():
     out = [
         ("kat_chain6", chain_design(6, arc_delay=1.25), None, False),
@@ -203,6 +304,14 @@ def cases():
         ("gen_uniform_tree", generate_design(GeneratorConfig(
             num_cells=300, fanout=uniform(1, 9), depth_target=7, seed=5,
             net_topology="random_tree")), None, True),
+        ("multi_out", multi_out_design(), None, True),
+        ("gen_multi_out_50k", add_multi_out_arcs(generate_design(GeneratorConfig(
+            num_cells=12500, fanout=power_law(2.0, 64), depth_target=20, seed=13)), seed=13),
+         None, False),
+        ("gen_multi_out_tree", add_multi_out_arcs(generate_design(GeneratorConfig(
+            num_cells=1500, fanout=power_law(2.0, 200), depth_target=10, seed=17,
+            net_topology="random_tree")), seed=17, frac=0.3, wide=(130,), loops=(4, 7)),
+         None, True),
     ]
     return out
 
@@ -242,7 +351,10 @@ def dump(name, design, gamma, softplus):
 
 if __name__ == "__main__":
     total = 0
+    only = set(sys.argv[1:])
     for name, d, gamma, sp in cases():
+        if only and name not in only:
+            continue
         n = dump(name, d, gamma, sp)
         sz = os.path.getsize(os.path.join(HERE, name + ".npz"))
         total += sz

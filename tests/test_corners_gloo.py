@@ -89,18 +89,18 @@ def test_gloo_world2_batch_reduction(tmp_path, name):
     np.testing.assert_allclose(got["d_edge"].numpy(), sum(r[2] for r in ref).numpy(), rtol=1e-12)
 
 
-def _cand_worker(rank, world, port, out):
+def _cand_worker(rank, world, port, out, n=6):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path[:0] = [here, os.path.dirname(here)]
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        mine = CO.corners_of_rank(6, rank, world)
+        mine = CO.corners_of_rank(n, rank, world)
         summ = torch.stack([torch.tensor([-1.0 * c, -0.1 * c, 10.0 - c], dtype=torch.float64)
                             for c in mine])
         dxy = torch.stack([torch.full((5, 2), float(c), dtype=torch.float64) for c in mine])
-        s, g = CO.gather_candidates(summ, dxy)
+        s, g = CO.gather_candidates(summ, dxy, n_candidates=n)
         if rank == 0:
             torch.save({"s": s, "g": g, "best": CO.best_candidate(s)}, out)
     finally:
@@ -116,3 +116,15 @@ def test_gloo_world2_candidate_gather(tmp_path):
     assert got["s"][:, 0].tolist() == [-float(c) for c in range(6)]
     assert all(float(got["g"][c, 0, 0]) == float(c) for c in range(6))
     assert got["best"] == 5
+
+
+def test_gloo_world2_candidate_gather_uneven(tmp_path):
+    """5 candidates on 2 ranks (3 + 2): rank 1 pads to 3 rows so the
+    all_gather shapes agree; the result is the 5 candidates in order."""
+    out = str(tmp_path / "c5.pt")
+    mp.spawn(_cand_worker, args=(2, _free_port(), out, 5), nprocs=2, join=True)
+    got = torch.load(out)
+    assert got["s"].shape == (5, 3) and got["g"].shape == (5, 5, 2)
+    assert got["s"][:, 0].tolist() == [-float(c) for c in range(5)]
+    assert all(float(got["g"][c, 0, 0]) == float(c) for c in range(5))
+    assert got["best"] == 4

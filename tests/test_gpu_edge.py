@@ -112,3 +112,29 @@ def test_nan_endpoint_requirement():
     epr[1, 1] = np.nan                         # early fall of the second
     raw.ep_required = epr
     _check_modes(raw.normalized())
+
+
+@pytest.mark.parametrize("name", ["multi_out", "gen_multi_out_tree", "gen_multi_out_50k"])
+def test_multi_out_arcs_every_mode(name):
+    """Pins with 2+ out-arcs (multi-output cells, a free PI and a feedthrough
+    root fanning out into several cells, out-arcs landing in nets of
+    different levels): the required-time fold and the gather-form adjoint
+    over out-arcs 2+ (diff.py:236-241 scatters them with np.add.at) in every
+    run mode, against the oracle and the reference's own outputs."""
+    from golden_util import load, raw_of
+    g = load(name)
+    raw = raw_of(g)
+    flat = _check_modes(raw, gamma=float(g["gamma"]))
+    assert int(np.diff(flat.mem_out_ptr).max()) >= 2
+    dev = ws.DeviceDesign(raw)
+    for flags in MODES.values():
+        dev.run(flags, gamma=float(g["gamma"]))
+        for f in ST_FIELDS:
+            assert np.array_equal(dev.get(f), g["st_" + f]), f
+        for f in G_FIELDS:
+            assert grad_close(dev.get(f), g["g_" + f]), f
+    if "gs_loss" in g:
+        dev.run(MODES["fused"], gamma=float(g["gamma"]), loss="softplus")
+        for f in G_FIELDS:
+            assert grad_close(dev.get(f), g["gs_" + f]), f
+    dev.close()

@@ -205,3 +205,16 @@ def test_descend_reduces_the_timing_loss():
     assert losses[-1] < losses[0]
     assert min(losses[1:]) < losses[0]
     dev.close()
+
+
+@pytest.mark.parametrize("name", ["multi_out", "gen_multi_out_tree", "gen_multi_out_50k"])
+@pytest.mark.parametrize("loss", ["hinge", "softplus"])
+def test_place_multi_out_arcs(name, loss):
+    """Position gradients on pins with several out-arcs (the slew adjoint
+    gsa of every out-arc is summed into its source pin)."""
+    raw = raw_of(load(name))
+    pl = PL.synthetic_placement(raw, seed=7)
+    dev = ws.DeviceDesign(raw)
+    PL.PlacementTimer(dev, pl, loss=loss).step()
+    check(dev, 0, raw, pl, loss)
+    dev.close()

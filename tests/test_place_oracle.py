@@ -132,7 +132,8 @@ def test_wire_model_identity_and_lengths():
 
 @pytest.mark.parametrize("name", ["kat_chain6", "kat_diamond", "kat_two_input", "kat_tie_break",
                                   "kat_flat_nets", "gen_tree_1200", "gen_heavy_1500",
-                                  "gen_single_in", "gen_uniform_tree"])
+                                  "gen_single_in", "gen_uniform_tree", "multi_out",
+                                  "gen_multi_out_tree"])
 def test_position_gradient_fd_golden_designs(name):
     """FD pinning on the reference's own test designs (the golden fixtures'
     netlists, softplus loss so every endpoint contributes)."""
