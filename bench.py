@@ -503,6 +503,9 @@ def main():
     if share:
         local = 0
     torch.cuda.set_device(local)
+    # one explicit stream for everything the bench enqueues (flush, events,
+    # engine passes, collectives): nothing can reorder around the timed work
+    torch.cuda.set_stream(torch.cuda.Stream())
     dist = None
     if world > 1:
         import torch.distributed as dist

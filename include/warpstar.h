@@ -98,7 +98,11 @@ enum ws_state_field {
     WS_F_D_ROOT_CAP = 16,               /* (N,2) dL/droot_cap (= dL/dload of the root) */
     WS_F_D_SLEW = 17,                   /* (P,2) dL/dslew */
     WS_F_D_LEN = 18,                    /* (M,)  dL/dlength of each member edge */
-    WS_F_D_XY = 19                      /* (P,2) dL/dx, dL/dy */
+    WS_F_D_XY = 19,                     /* (P,2) dL/dx, dL/dy */
+    /* batch gradients of the last WS_RUN_CORNER_SUM run (the corner argument
+     * is ignored: one per context) */
+    WS_F_D_ARC_SUM = 20,                /* (A,2) sum over the run's corners of d_arc */
+    WS_F_D_EDGE_SUM = 21                /* (M,2) sum over the run's corners of d_edge */
 };
 
 /* topology arrays (ws_get_topology); int64 on the host like FlatDesign */
@@ -129,8 +133,11 @@ enum ws_run_flags {
     WS_RUN_WIRE = 512u,      /* first: mem_res / mem_cap from the positions (WS_V_XY ...) */
     WS_RUN_POSGRAD = 1024u,  /* last (needs HARD|LSE|GRAD in the same call): slew / load
                                 adjoint sweep, Elmore adjoint, dL/dxy */
-    WS_RUN_TIMED = 2048u     /* sequential or fused mode, no graph: a CUDA event after every
+    WS_RUN_TIMED = 2048u,    /* sequential or fused mode, no graph: a CUDA event after every
                                 launch, read back with ws_kernel_times (measured costs) */
+    WS_RUN_CORNER_SUM = 4096u /* with GRAD, n_corners <= 16: also sum_k d_arc and sum_k d_edge
+                                over the run's corners (WS_F_D_ARC_SUM / WS_F_D_EDGE_SUM), the
+                                gradient of the batch objective sum_k loss_k */
 };
 
 enum ws_loss_kind { WS_LOSS_HINGE = 0, WS_LOSS_SOFTPLUS = 1 };

@@ -25,13 +25,15 @@ V_XY, V_RES0, V_CAP0, V_WIRE = range(7, 11)
 (F_LOAD, F_NET_DELAY, F_IMPULSE, F_SLEW, F_ARRIVAL, F_REQUIRED, F_SLACK, F_ARC_DELAY,
  F_LSE_ARRIVAL, F_ARC_WEIGHTS, F_D_ARC, F_D_EDGE, F_ADJOINT, F_SUMMARY) = range(14)
 F_D_RES, F_D_CAP, F_D_ROOT_CAP, F_D_SLEW, F_D_LEN, F_D_XY = range(14, 20)
+F_D_ARC_SUM, F_D_EDGE_SUM = 20, 21
 STATE_FIELDS = {"load": F_LOAD, "net_delay": F_NET_DELAY, "impulse": F_IMPULSE, "slew": F_SLEW,
                 "arrival": F_ARRIVAL, "required": F_REQUIRED, "slack": F_SLACK,
                 "arc_delay": F_ARC_DELAY, "lse_arrival": F_LSE_ARRIVAL,
                 "arc_weights": F_ARC_WEIGHTS, "d_arc": F_D_ARC, "d_edge": F_D_EDGE,
                 "adjoint": F_ADJOINT, "summary": F_SUMMARY,
                 "d_res": F_D_RES, "d_cap": F_D_CAP, "d_root_cap": F_D_ROOT_CAP,
-                "d_slew": F_D_SLEW, "d_len": F_D_LEN, "d_xy": F_D_XY}
+                "d_slew": F_D_SLEW, "d_len": F_D_LEN, "d_xy": F_D_XY,
+                "d_arc_sum": F_D_ARC_SUM, "d_edge_sum": F_D_EDGE_SUM}
 VALUE_FIELDS = {"mem_res": V_MEM_RES, "mem_cap": V_MEM_CAP, "root_cap": V_ROOT_CAP,
                 "lut_t_flat": V_LUT_T, "pi_arrival": V_PI_ARRIVAL, "pi_slew": V_PI_SLEW,
                 "ep_required": V_EP_REQUIRED, "xy": V_XY, "res0": V_RES0, "cap0": V_CAP0,
@@ -47,6 +49,7 @@ RUN_HARD, RUN_LSE, RUN_GRAD, RUN_TWO_STREAM, RUN_FUSED, RUN_GRAPH, RUN_SUMMARY, 
     1, 2, 4, 8, 16, 32, 64, 128)
 RUN_PERSISTENT = 256
 RUN_WIRE, RUN_POSGRAD, RUN_TIMED = 512, 1024, 2048
+RUN_CORNER_SUM = 4096
 LOSS_KINDS = {"hinge": 0, "softplus": 1}
 DIMS_LEN = 11
 

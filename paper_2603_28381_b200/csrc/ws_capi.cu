@@ -102,12 +102,29 @@ int64_t state_len(const ws::Context& c, int field)
     case WS_F_D_ROOT_CAP: return 2ll * t.N;
     case WS_F_D_SLEW: case WS_F_D_XY: return 2ll * t.P;
     case WS_F_D_LEN: return t.M;
+    case WS_F_D_ARC_SUM: return 2ll * t.A;
+    case WS_F_D_EDGE_SUM: return 2ll * t.M;
     default: throw ws::Error(WS_ERR_VALUE, "unknown state field");
     }
 }
 
+// the batch-gradient buffers (zeroed once: entries of arcs that feed no net
+// root are never written by a pass)
+void ensure_dsum(ws::Context& c)
+{
+    if (c.dsum_arc) return;
+    c.dsum_arc = c.val_mem.alloc<double>(2 * (size_t)c.t.A);
+    c.dsum_edge = c.val_mem.alloc<double>(2 * (size_t)c.t.M);
+    WS_CUDA(cudaMemset(c.dsum_arc, 0, sizeof(double) * 2 * (size_t)std::max(c.t.A, 1)));
+    WS_CUDA(cudaMemset(c.dsum_edge, 0, sizeof(double) * 2 * (size_t)std::max(c.t.M, 1)));
+}
+
 double* state_ptr(ws::Context& c, int corner, int field)
 {
+    if (field == WS_F_D_ARC_SUM || field == WS_F_D_EDGE_SUM) {
+        ensure_dsum(c);
+        return field == WS_F_D_ARC_SUM ? c.dsum_arc : c.dsum_edge;
+    }
     if (field >= WS_F_D_RES && field <= WS_F_D_XY) {
         ws::place_enable(c);
         ws::PlaceCorner& g = c.place[corner];
@@ -146,61 +163,82 @@ cudaStream_t as_stream(void* s, cudaStream_t dflt) { return s ? static_cast<cuda
 
 namespace ws {
 
-void alloc_corner(Context& ctx, CornerSlot& cs)
+// Every corner's copy of a field lives in ONE allocation at a uniform stride
+// (corner k = corner 0 + k * stride), so a kernel that maps corners onto
+// lanes (the corner-batched level kernels) derives a lane's pointers from
+// corner 0's with one multiply-add instead of loading a pointer table.
+void alloc_corners(Context& ctx, int n)
 {
     const Topo& t = ctx.t;
     Arena& ar = ctx.val_mem;
-    Corner& d = cs.d;
-    d.mem_res = ar.alloc<double>(4 * (size_t)t.M);
-    d.mem_cap = ar.alloc<double>(4 * (size_t)t.M);
-    d.root_cap = ar.alloc<double>(4 * (size_t)t.N);
-    d.lut_t_flat = ar.alloc<double>((size_t)ctx.lut_t_len);
-    d.pi_arrival = ar.alloc<double>(4 * (size_t)t.I);
-    d.pi_slew = ar.alloc<double>(4 * (size_t)t.I);
-    d.ep_required = ar.alloc<double>(4 * (size_t)t.E);
-    d.load = ar.alloc<double>(4 * (size_t)t.P);
-    d.net_delay = ar.alloc<double>(4 * (size_t)t.P);
-    d.impulse = ar.alloc<double>(4 * (size_t)t.P);
-    d.slew = ar.alloc<double>(4 * (size_t)t.P);
-    d.arrival = ar.alloc<double>(4 * (size_t)t.P);
-    d.required = ar.alloc<double>(4 * (size_t)t.P);
-    d.slack = ar.alloc<double>(4 * (size_t)t.P);
-    d.arc_delay = ar.alloc<double>(4 * (size_t)t.A);
-    d.lse_at = ar.alloc<double>(2 * (size_t)t.P);
-    d.weights = ar.alloc<double>(2 * (size_t)t.A);
-    d.d_arc = ar.alloc<double>(2 * (size_t)t.A);
-    d.d_edge = ar.alloc<double>(2 * (size_t)t.M);
-    d.adjoint = ar.alloc<double>(2 * (size_t)t.P);
-    // tree-net RC scratch only when the design has RC trees (or w != 8 is
-    // requested later: allocated lazily then)
-    d.mem_buf = nullptr;
-    d.mem_dbuf = nullptr;
+    CornerStrides& st = ctx.cstride;
+    st.P4 = 4 * (long long)t.P; st.P2 = 2 * (long long)t.P;
+    st.A4 = 4 * (long long)t.A; st.A2 = 2 * (long long)t.A;
+    st.M4 = 4 * (long long)t.M; st.M2 = 2 * (long long)t.M;
+    st.N4 = 4 * (long long)t.N; st.LT = ctx.lut_t_len;
+    st.I4 = 4 * (long long)t.I; st.E4 = 4 * (long long)t.E;
     const int nl = ctx.tns_plan ? std::max(1, ctx.tns_plan->n_leaves) : 1;
-    d.red_tmp = ar.alloc<double>(3 * (size_t)(2 * nl));
-    d.summary = ar.alloc<double>(4);
-    d.sync_ctr = ar.alloc<unsigned>(4);
-    WS_CUDA(cudaMemset(d.sync_ctr, 0, 4 * sizeof(unsigned)));
-    d.big_part = ar.alloc<double>(8 * (size_t)std::max(t.n_parts, 1));
-    d.big_ctr = ar.alloc<unsigned>(4 * (size_t)std::max(t.n_big, 1));
-    WS_CUDA(cudaMemset(d.big_ctr, 0, 4 * sizeof(unsigned) * (size_t)std::max(t.n_big, 1)));
+    st.RT = 3 * (long long)(2 * nl);
+    st.BP = 8 * (long long)std::max(t.n_parts, 1);
+    st.BC = 4 * (long long)std::max(t.n_big, 1);
+    ctx.corners.resize(n);
+    auto block = [&](long long len, double* Corner::*f, bool zero) {
+        double* b = ar.alloc<double>((size_t)n * (size_t)std::max(len, 1ll));
+        if (zero) WS_CUDA(cudaMemset(b, 0, sizeof(double) * (size_t)n * (size_t)std::max(len, 1ll)));
+        for (int k = 0; k < n; k++) ctx.corners[k].d.*f = b + (size_t)k * (size_t)len;
+    };
+    block(st.M4, &Corner::mem_res, false);
+    block(st.M4, &Corner::mem_cap, false);
+    block(st.N4, &Corner::root_cap, false);
+    block(st.LT, &Corner::lut_t_flat, false);
+    block(st.I4, &Corner::pi_arrival, false);
+    block(st.I4, &Corner::pi_slew, false);
+    block(st.E4, &Corner::ep_required, false);
+    block(st.P4, &Corner::load, false);
+    block(st.P4, &Corner::net_delay, false);
+    block(st.P4, &Corner::impulse, false);
+    block(st.P4, &Corner::slew, false);
+    block(st.P4, &Corner::arrival, false);
+    block(st.P4, &Corner::required, false);
     // arrays that are not fully rewritten by every pass start defined
-    WS_CUDA(cudaMemset(d.arc_delay, 0, sizeof(double) * 4 * (size_t)std::max(t.A, 1)));
-    WS_CUDA(cudaMemset(d.weights, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));
-    WS_CUDA(cudaMemset(d.d_arc, 0, sizeof(double) * 2 * (size_t)std::max(t.A, 1)));
-    WS_CUDA(cudaMemset(d.d_edge, 0, sizeof(double) * 2 * (size_t)std::max(t.M, 1)));
-    WS_CUDA(cudaMemset(d.lse_at, 0, sizeof(double) * 2 * (size_t)std::max(t.P, 1)));
-    WS_CUDA(cudaMemset(d.adjoint, 0, sizeof(double) * 2 * (size_t)std::max(t.P, 1)));
-    WS_CUDA(cudaMemset(d.slack, 0, sizeof(double) * 4 * (size_t)std::max(t.P, 1)));
-    WS_CUDA(cudaMemset(d.summary, 0, sizeof(double) * 4));
+    block(st.P4, &Corner::slack, true);
+    block(st.A4, &Corner::arc_delay, true);
+    block(st.P2, &Corner::lse_at, true);
+    block(st.A2, &Corner::weights, true);
+    block(st.A2, &Corner::d_arc, true);
+    block(st.M2, &Corner::d_edge, true);
+    block(st.P2, &Corner::adjoint, true);
+    block(st.RT, &Corner::red_tmp, false);
+    block(4, &Corner::summary, true);
+    block(st.BP, &Corner::big_part, false);
+    {
+        unsigned* sc = ar.alloc<unsigned>((size_t)n * 4);
+        WS_CUDA(cudaMemset(sc, 0, sizeof(unsigned) * (size_t)n * 4));
+        unsigned* bc = ar.alloc<unsigned>((size_t)n * (size_t)st.BC);
+        WS_CUDA(cudaMemset(bc, 0, sizeof(unsigned) * (size_t)n * (size_t)st.BC));
+        for (int k = 0; k < n; k++) {
+            Corner& d = ctx.corners[k].d;
+            d.sync_ctr = sc + 4 * (size_t)k;
+            d.big_ctr = bc + (size_t)k * (size_t)st.BC;
+            // tree-net RC scratch only when the design has RC trees (or w != 8
+            // is requested later: allocated lazily then)
+            d.mem_buf = nullptr;
+            d.mem_dbuf = nullptr;
+        }
+    }
 }
 
 void ensure_tree_scratch(Context& ctx)
 {
-    for (auto& cs : ctx.corners)
-        if (!cs.d.mem_buf) {
-            cs.d.mem_buf = ctx.val_mem.alloc<double>(4 * (size_t)ctx.t.M);
-            cs.d.mem_dbuf = ctx.val_mem.alloc<double>(4 * (size_t)ctx.t.M);
+    if (!ctx.corners.empty() && !ctx.corners[0].d.mem_buf) {
+        const size_t n = ctx.corners.size(), len = 4 * (size_t)ctx.t.M;
+        double* b = ctx.val_mem.alloc<double>(n * len);
+        double* db = ctx.val_mem.alloc<double>(n * len);
+        for (size_t k = 0; k < n; k++) {
+            ctx.corners[k].d.mem_buf = b + k * len;
+            ctx.corners[k].d.mem_dbuf = db + k * len;
         }
+    }
     std::vector<Corner> v;
     for (auto& cs : ctx.corners) v.push_back(cs.d);
     WS_CUDA(cudaMemcpy(ctx.d_corners, v.data(), sizeof(Corner) * v.size(), cudaMemcpyHostToDevice));
@@ -253,8 +291,7 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
         WS_CUDA(cudaStreamCreateWithFlags(&c.s_grad, cudaStreamDefault));
         ws::build_topology(c, d);
         ws::summary_plan_init(c);
-        c.corners.resize(n_corners);
-        for (auto& cs : c.corners) ws::alloc_corner(c, cs);
+        ws::alloc_corners(c, n_corners);
         for (int k = 0; k < n_corners; k++) ws::upload_values(c, k, d);
         c.d_corners = c.topo_mem.alloc<ws::Corner>(n_corners);
         ws::ensure_tree_scratch(c);   // tree-net RC and big-net fold scratch
@@ -385,6 +422,13 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
         if ((flags & WS_RUN_POSGRAD) && (flags & WS_RUN_PERSISTENT))
             throw ws::Error(WS_ERR_VALUE, "WS_RUN_POSGRAD is not available with WS_RUN_PERSISTENT");
         if (flags & (WS_RUN_WIRE | WS_RUN_POSGRAD)) ws::place_enable(c);
+        if (flags & WS_RUN_CORNER_SUM) {
+            if (!(flags & WS_RUN_GRAD))
+                throw ws::Error(WS_ERR_STATE, "WS_RUN_CORNER_SUM needs WS_RUN_GRAD in the same run");
+            if (n_corners > 16)
+                throw ws::Error(WS_ERR_VALUE, "WS_RUN_CORNER_SUM sums at most 16 corners per run");
+            ensure_dsum(c);
+        }
         if (flags & WS_RUN_GRAPH) {
             const unsigned key = flags & ~WS_RUN_GRAPH;
             cudaGraphExec_t exec = nullptr;

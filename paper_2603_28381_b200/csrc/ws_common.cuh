@@ -138,6 +138,31 @@ struct Corner {
     unsigned *big_ctr;   // [n_big * 4] last-chunk-done counters (rc, hard, grad, fused)
 };
 
+// Per-field distance (in elements) between consecutive corners' copies: every
+// corner's copy of a field is one allocation (ws_capi.cu alloc_corners).
+struct CornerStrides {
+    long long P4, P2, A4, A2, M4, M2, N4, LT, I4, E4, RT, BP, BC;
+};
+
+// corner c0 + k of a batch whose corner c0 is `c`
+__host__ __device__ __forceinline__ Corner corner_at(const Corner& c, const CornerStrides& s, int k)
+{
+    Corner r = c;
+    const long long kk = k;
+    r.mem_res += kk * s.M4; r.mem_cap += kk * s.M4; r.root_cap += kk * s.N4;
+    r.lut_t_flat += kk * s.LT; r.pi_arrival += kk * s.I4; r.pi_slew += kk * s.I4;
+    r.ep_required += kk * s.E4;
+    r.load += kk * s.P4; r.net_delay += kk * s.P4; r.impulse += kk * s.P4; r.slew += kk * s.P4;
+    r.arrival += kk * s.P4; r.required += kk * s.P4; r.slack += kk * s.P4;
+    r.arc_delay += kk * s.A4;
+    r.lse_at += kk * s.P2; r.weights += kk * s.A2; r.d_arc += kk * s.A2; r.d_edge += kk * s.M2;
+    r.adjoint += kk * s.P2;
+    r.red_tmp += kk * s.RT; r.summary += kk * 4; r.sync_ctr += kk * 4;
+    r.big_part += kk * s.BP; r.big_ctr += kk * s.BC;
+    if (r.mem_buf) { r.mem_buf += kk * s.M4; r.mem_dbuf += kk * s.M4; }   // tree-net scratch
+    return r;
+}
+
 struct LutView {
     const int *s_ptr, *l_ptr, *t_ptr;
     const double *s, *l, *t;

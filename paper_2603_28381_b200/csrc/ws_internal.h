@@ -119,6 +119,8 @@ struct CornerSlot {
 
 struct Context {
     Topo t{};
+    CornerStrides cstride{};          // corner k's field = corner 0's + k * stride
+    double *dsum_arc = nullptr, *dsum_edge = nullptr;   // WS_RUN_CORNER_SUM outputs (A,2) (M,2)
     Arena topo_mem;
     Arena val_mem;
     Scratch scratch;
@@ -155,7 +157,7 @@ struct Context {
 };
 
 void build_topology(Context& ctx, const ws_design_desc* d);
-void alloc_corner(Context& ctx, CornerSlot& cs);
+void alloc_corners(Context& ctx, int n);
 void upload_values(Context& ctx, int corner, const ws_design_desc* d);
 void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int loss_kind,
               int granularity, cudaStream_t s, cudaStream_t g, int w);

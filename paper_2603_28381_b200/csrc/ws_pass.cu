@@ -42,6 +42,9 @@ namespace ws {
 #ifndef WS_MINB
 #define WS_MINB 2   // min resident blocks per SM of the level kernels
 #endif
+#ifndef WS_MINB_BATCH
+#define WS_MINB_BATCH 4   // ... of the fused level kernels in corner batches (>= 4 corners)
+#endif
 
 constexpr int MAXC = 16;   // corners per launch (blockIdx.y)
 struct Corners {
@@ -1048,6 +1051,31 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
     __syncthreads();                         // smem reusable by the next task
 }
 
+// sum over the corners of a batch, in corner order (WS_RUN_CORNER_SUM): the
+// gradient of the batch objective sum_k loss_k.  Every corner's copy of a
+// field sits at a uniform stride from corner c0's (alloc_corners).
+__global__ void k_corner_sum(Corner c0, CornerStrides cst, int A, int M, int nc, double* dsum_arc,
+                             double* dsum_edge)
+{
+    pdl_trigger();
+    pdl_wait();
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const double* src;
+    long long stride;
+    double* dst;
+    if (i < 2 * (size_t)A) {
+        src = c0.d_arc + i; stride = cst.A2; dst = dsum_arc + i;
+    } else if (i < 2 * (size_t)A + 2 * (size_t)M) {
+        const size_t e = i - 2 * (size_t)A;
+        src = c0.d_edge + e; stride = cst.M2; dst = dsum_edge + e;
+    } else {
+        return;
+    }
+    double tot = src[0];
+    for (int k = 1; k < nc; k++) tot = __dadd_rn(tot, src[(size_t)k * stride]);
+    *dst = tot;
+}
+
 // ---- streaming RC (reduce width 8) --------------------------------------
 // The RC stage has no level dependencies, so it runs as one HBM-streaming
 // launch instead of per-task blocks: member blocks take RC_ITEMS
@@ -1237,8 +1265,11 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w)
     rc_body(t, cs.c[blockIdx.y], T, S, R, w);
 }
 
-template <bool HARD, bool LSE>
-__global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
+// MB: min resident blocks per SM.  Single corners are latency-bound on the
+// level chain (2: the full register budget); corner batches are
+// throughput-bound and run a 4-block variant (WS_MINB_BATCH).
+template <bool HARD, bool LSE, int MB = WS_MINB>
+__global__ void __launch_bounds__(PASS_TPB, MB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
                                                      bool use_smem, double g)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1259,8 +1290,8 @@ __global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_fwd(Topo t, LutSrc ls, Co
     LSTAMP(3);
 }
 
-template <bool HARD, bool GRAD>
-__global__ void __launch_bounds__(PASS_TPB, WS_MINB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
+template <bool HARD, bool GRAD, int MB = WS_MINB>
+__global__ void __launch_bounds__(PASS_TPB, MB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
                                                      int variant)
 {
     __shared__ BwdSmem S;
@@ -2277,8 +2308,12 @@ struct Launcher {
     {
         const int nt = tasks(li);
         if (nt <= 0) return;
-        launch(k_fwd<H, Lse>, dim3(nt, nc), dim3(PASS_TPB), H ? lut_bytes : 0, s, probed(nt), ls, cs,
-               ctx.lvt_ptr_host[li], use_smem, g);
+        if (H && Lse && nc >= 4)
+            launch(k_fwd<H, Lse, WS_MINB_BATCH>, dim3(nt, nc), dim3(PASS_TPB), lut_bytes, s, probed(nt), ls,
+                   cs, ctx.lvt_ptr_host[li], use_smem, g);
+        else
+            launch(k_fwd<H, Lse>, dim3(nt, nc), dim3(PASS_TPB), H ? lut_bytes : 0, s, probed(nt), ls, cs,
+                   ctx.lvt_ptr_host[li], use_smem, g);
         count++;
     }
     template <bool H, bool G>
@@ -2287,8 +2322,21 @@ struct Launcher {
         const int nt = tasks(li);
         if (nt <= 0) return;
         const int variant = H && G ? 3 : (H ? 1 : 2);
-        launch(k_bwd<H, G>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs, ctx.lvt_ptr_host[li],
-               g, kind, variant);
+        if (H && G && nc >= 4)
+            launch(k_bwd<H, G, WS_MINB_BATCH>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs,
+                   ctx.lvt_ptr_host[li], g, kind, variant);
+        else
+            launch(k_bwd<H, G>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs, ctx.lvt_ptr_host[li],
+                   g, kind, variant);
+        count++;
+    }
+    // sum_k d_arc / d_edge over the batch
+    void corner_sum(cudaStream_t s)
+    {
+        const size_t n = 2 * ((size_t)ctx.t.A + (size_t)ctx.t.M);
+        if (!n) return;
+        launch(k_corner_sum, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, cs.c[0], ctx.cstride,
+               ctx.t.A, ctx.t.M, nc, ctx.dsum_arc, ctx.dsum_edge);
         count++;
     }
     void fin(cudaStream_t s, double g, int kind)
@@ -2391,6 +2439,8 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
     if (la.lut_bytes > 48 * 1024) {
         WS_CUDA(cudaFuncSetAttribute(k_fwd<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la.lut_bytes));
         WS_CUDA(cudaFuncSetAttribute(k_fwd<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la.lut_bytes));
+        WS_CUDA(cudaFuncSetAttribute(k_fwd<true, true, WS_MINB_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)la.lut_bytes));
     }
     const bool hard = flags & WS_RUN_HARD, lse = flags & WS_RUN_LSE, grad = flags & WS_RUN_GRAD;
     const bool fused = (flags & WS_RUN_FUSED) && hard && lse && grad;
@@ -2401,6 +2451,7 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         la.rc(s, w);
         if (lse) la.persistent<true, true>(s, w, g, kind);
         else la.persistent<false, false>(s, w, g, kind);
+        if (lse && (flags & WS_RUN_CORNER_SUM)) la.corner_sum(s);
     } else if (fused) {
         // WS_RUN_TIMED: kinds 0 RC, 1 fused forward+LSE level, 2 fused
         // backward+gradient level, 5 tail (the events serialise the PDL overlap)
@@ -2418,6 +2469,7 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
             la.mark(s, 2, li);
         }
         la.fin_summary(s, g, kind);
+        if (flags & WS_RUN_CORNER_SUM) la.corner_sum(s);
         la.mark(s, 5, -1);
     } else if (two) {
         // stream S: the hard pass; stream G: LSE + gradients, gated per
@@ -2454,6 +2506,7 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         WS_CUDA(cudaEventRecord(ev[n_groups + 1], gs));   // join
         WS_CUDA(cudaStreamWaitEvent(s, ev[n_groups + 1], 0));
         la.summary(s, g, kind, grad, true);
+        if (grad && (flags & WS_RUN_CORNER_SUM)) la.corner_sum(s);
     } else {
         // kinds of fusion.py's KernelGraph: 0 net_rc, 1 cell_delay_at,
         // 2 slack_bwd, 3 lse_fwd, 4 grad_bwd, 5 other
@@ -2492,6 +2545,7 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         if (!hard && (flags & WS_RUN_SLACK)) la.slack_all(s);
         if (hard || grad || (flags & WS_RUN_SUMMARY))
             la.summary(s, g, kind, grad, hard || (flags & WS_RUN_SUMMARY));
+        if (grad && (flags & WS_RUN_CORNER_SUM)) la.corner_sum(s);
         la.mark(s, 5, -1);
     }
     WS_CHECK_LAUNCH();

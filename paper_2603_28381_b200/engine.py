@@ -202,9 +202,9 @@ class DeviceDesign:
             return (self.n_arcs, 4)
         if name in ("lse_arrival", "adjoint"):
             return (self.n_pins, 2)
-        if name in ("arc_weights", "d_arc"):
+        if name in ("arc_weights", "d_arc", "d_arc_sum"):
             return (self.n_arcs, 2)
-        if name == "d_edge":
+        if name in ("d_edge", "d_edge_sum"):
             return (self.n_members, 2)
         if name == "summary":
             return (3,)

@@ -234,7 +234,7 @@ def _topo_key(flat):
     return tuple(id(getattr(flat, k)) for k in _TOPO_KEYS)
 
 
-def device_of(flat) -> DeviceDesign:
+def device_of(flat, upload_values: bool = True) -> DeviceDesign:
     """The device context of a FlatDesign with the flat's CURRENT value arrays
     uploaded (callers may substitute mem_res/mem_cap/... as the reference's
     copy.copy(flat) workflow does).  Rebinding an index array
@@ -249,7 +249,7 @@ def device_of(flat) -> DeviceDesign:
             flat._dev_key = key
         except AttributeError:
             pass
-    else:
+    elif upload_values:
         dev.set_values(0, mem_res=flat.mem_res, mem_cap=flat.mem_cap, root_cap=flat.root_cap,
                        lut_t_flat=flat.lut_t_flat, pi_arrival=flat.pi_arrival,
                        pi_slew=flat.pi_slew, ep_required=flat.ep_required)

@@ -64,11 +64,28 @@ class TimingState:
 
 
 def _summary(state: TimingState, flat):
+    """(TNS, WNS) of ``state.slack`` by the device summary kernel.  Only the
+    slack goes up (no value re-upload), and corner 0's own device slack is
+    restored afterwards (device-to-device), so zero-copy views of the last
+    pass stay valid."""
+    import torch
     from .flatten import device_of
-    dev = device_of(flat)
+    dev = device_of(flat, upload_values=False)
+    keep = dev.tensor("slack").clone()
     dev.set_state(0, slack=state.slack)
     dev.run(_lib.RUN_SUMMARY)
-    return dev.summary(0)
+    out = dev.summary(0)
+    dev.tensor("slack").copy_(keep)
+    torch.cuda.current_stream().synchronize()
+    return out
+
+
+def tns_wns(state: TimingState, flat):
+    """(TNS, WNS) from one device summary run."""
+    if not len(flat.ep_pin):
+        return 0.0, float("inf")
+    t, w, _ = _summary(state, flat)
+    return t, w
 
 
 def tns(state: TimingState, flat) -> float:
