@@ -6,17 +6,20 @@
 One step = one full differentiable STA pass over the synthetic superblue-shaped
 C3 netlist (2,490,236 pins): init, RC, 60 forward levels with
 the LSE smooth forward, endpoint hinge loss, 60 backward levels with the
-gradient adjoint, slack, TNS/WNS — inputs resident in HBM.  Under torchrun
-(N>1) every rank runs its own corner of the C5 corner set (corner k = rank,
-weak scaling) and the ranks all-reduce WNS (MIN), TNS and loss (SUM) and the
-gradients d_arc/d_edge (SUM) over NCCL each step.
+gradient adjoint, slack, TNS/WNS — inputs resident in HBM, one explicit CUDA
+stream for everything the bench enqueues.  Under torchrun (N>1) every rank
+runs its own corner of the C5 corner set (corner k = rank, weak scaling) and
+the batch objective's exchange (WNS MIN, TNS / loss SUM, d_arc / d_edge SUM)
+runs over NCCL on a side stream, overlapped with the next pass.
 
-value = whole-job ms per pass = max-over-ranks device time of K steps / (K*N).
-``e2e`` is the same pass through the public API with the step's value inputs
-(mem_res, mem_cap, root_cap) copied from pinned host memory and TNS/WNS/loss
-read back every step.  ``--impl reference`` times the reference's own CPU
-implementation (stasim run_engine + timing_gradients, from oracle/_ref) on
-this host.
+value = whole-job ms per pass: the median per-pass device time (N = 1) or the
+max-over-ranks device time of K steps / (K * N).  ``e2e`` is the same pass
+through the public API with each step's RC inputs copied H2D from pinned host
+memory and the gradients (d_arc, d_edge) plus TNS/WNS/loss copied D2H every
+step; ``e2e_dropin`` is the reference's own plugin call, ``run_engine(flat)``
+then ``timing_gradients(flat, state=...)``, numpy in and out.  ``--impl
+reference`` times the reference's own CPU implementation (stasim run_engine +
+timing_gradients from baseline/_ref) on this host, pinned to one core.
 """
 
 from __future__ import annotations
@@ -114,21 +117,49 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (the --impl reference arm and the cpu_baseline object)
+# CPU reference (the --impl reference arm and the cpu_baseline objects)
 
-def reference_flat(raw):
+class OneCore:
+    """The CPU arm's measurement region: pinned to one core (taskset -c 0
+    equivalent) with BLAS/OpenMP pools limited to one thread (BASELINE.md §4;
+    the reference is single-threaded by construction)."""
+
+    def __enter__(self):
+        self.aff = os.sched_getaffinity(0)
+        self.core = min(self.aff)
+        os.sched_setaffinity(0, {self.core})
+        try:
+            from threadpoolctl import threadpool_limits
+            self.lim = threadpool_limits(1)
+        except Exception:
+            self.lim = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.lim is not None:
+            self.lim.unregister()
+        os.sched_setaffinity(0, self.aff)
+
+
+def reference_dir():
+    """The pip-installed unmodified reference (baseline/_ref),
+    else the same sources built by oracle/build_ref.sh."""
+    return next((d for d in (os.path.join(REPO, "baseline", "_ref"), os.path.join(REPO, "oracle", "_ref"))
+                 if os.path.isdir(os.path.join(d, "stasim"))), None)
+
+
+def reference_flat(raw, of=None):
     """The reference's FlatDesign for `raw`, assembled from the oracle's
     flatten (pinned bit-exact to the reference's flatten by
     tests/test_oracle_golden.py) — the reference's own flatten() would need
     ~100 s of Python object construction at C3."""
     from oracle import oracle as O
-    of = O.flatten_raw(raw)
-    # the pip-installed unmodified reference (baseline/_ref, see DESIGN.md §7),
-    # else the same sources built by oracle/build_ref.sh
-    ref = next((d for d in (os.path.join(REPO, "baseline", "_ref"), os.path.join(REPO, "oracle", "_ref"))
-                if os.path.isdir(os.path.join(d, "stasim"))), None)
+    if of is None:
+        of = O.flatten_raw(raw)
+    ref = reference_dir()
     if ref is not None:
-        sys.path.insert(0, ref)
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
         import stasim  # the unmodified reference
         from stasim.flatten import FlatDesign, LevelSchedule
         from stasim.backend import backend_name
@@ -139,88 +170,246 @@ def reference_flat(raw):
     return of, "port", "oracle/sta_oracle.c (C restatement)"
 
 
-def time_reference(raw, max_passes, budget_s):
-    flat, kind, what = reference_flat(raw)
+def _ref_pass_fn(flat, kind, hard_only=False):
     if kind == "reference":
         from stasim.warp import run_engine
         from stasim.diff import timing_gradients
 
         def one():
             st = run_engine(flat)
-            timing_gradients(flat, state=st)
+            if not hard_only:
+                timing_gradients(flat, state=st)
     else:
         from oracle import oracle as O
 
         def one():
             st = O.run_engine(flat)
-            O.timing_gradients(flat, st)
-    t0 = time.perf_counter()
-    one()                                   # warm-up (lazy level_view caches)
-    warm = time.perf_counter() - t0
-    n = int(max(1, min(max_passes, budget_s // max(warm, 1e-3))))
-    times = []
-    for _ in range(n):
+            if not hard_only:
+                O.timing_gradients(flat, st)
+    return one
+
+
+def time_cpu(fn, max_runs, budget_s):
+    """Median wall time of `fn` on one pinned core: one warm-up (the
+    reference's lazy level_view caches), then up to max_runs runs within
+    budget_s."""
+    with OneCore() as oc:
         t0 = time.perf_counter()
-        one()
-        times.append(time.perf_counter() - t0)
-    return {"ms": 1e3 * statistics.median(times), "passes": n, "kind": kind, "what": what,
+        fn()
+        warm = time.perf_counter() - t0
+        n = int(max(1, min(max_runs, budget_s // max(warm, 1e-3))))
+        times = []
+        for _ in range(n):
+            t0 = time.perf_counter()
+            fn()
+            times.append(time.perf_counter() - t0)
+    return {"ms": 1e3 * statistics.median(times), "runs": n, "core": oc.core,
             "times_ms": [round(1e3 * t, 1) for t in times]}
 
 
-def corner_batch(raw, rank, world, flags, steps, dist=None, n_total=16):
+def time_reference(raw, max_passes, budget_s, hard_only=False):
+    flat, kind, what = reference_flat(raw)
+    r = time_cpu(_ref_pass_fn(flat, kind, hard_only), max_passes, budget_s)
+    r.update(kind=kind, what=what)
+    return r
+
+
+# C5 on the host: a spawn pool of W workers, one corner per task (the
+# reference's bench process pool, bench.py:188-191)
+_POOL = {}
+
+
+def _pool_init(npz, ref):
+    import numpy as _np
+    sys.path[:0] = [REPO] + ([ref] if ref else [])
+    z = _np.load(npz, allow_pickle=False)
+    ns = type("NS", (), {})()
+    for k in z.files:
+        setattr(ns, k, z[k] if z[k].ndim else z[k].item())
+    lv_ptr = z["_levels_ptr"]
+    ns.levels = [z["_levels_nets"][lv_ptr[i]:lv_ptr[i + 1]] for i in range(len(lv_ptr) - 1)]
+    ns.level_of = z["_level_of"]
+    flat, kind, _ = reference_flat(None, of=ns)
+    _POOL.update(flat=flat, kind=kind)
+
+
+def _pool_corner(k):
+    import copy
+    base, kind = _POOL["flat"], _POOL["kind"]
+    fl = copy.copy(base)
+    fr, fc = 0.85 + 0.02 * k, 0.90 + 0.0125 * k
+    fl.mem_res = base.mem_res * fr
+    fl.mem_cap = base.mem_cap * fc
+    fl.root_cap = base.root_cap * fc
+    fl.lut_t_flat = base.lut_t_flat * fc
+    _ref_pass_fn(fl, kind)()
+    return k
+
+
+def cpu_corner_pool(raw, n_total=16):
+    """corners/s of the CPU reference on this host: W = min(16, cores)
+    worker processes (spawn), one C5 corner (copy.copy(flat) value
+    substitution) per task; a warm-up map, then the timed map
+    of all 16 corners."""
+    import multiprocessing as mp
+    import tempfile
+    from oracle import oracle as O
+    of = O.flatten_raw(raw)
+    arrs = {}
+    for k, v in vars(of).items():
+        if isinstance(v, np.ndarray):
+            arrs[k] = v
+        elif isinstance(v, (int, float, np.integer, np.floating)):
+            arrs[k] = np.asarray(v)
+    arrs["_levels_ptr"] = np.concatenate([[0], np.cumsum([len(x) for x in of.levels])]).astype(np.int64)
+    arrs["_levels_nets"] = (np.concatenate(of.levels) if of.levels else np.zeros(0)).astype(np.int64)
+    arrs["_level_of"] = np.asarray(of.level_of)
+    w = max(1, min(n_total, len(os.sched_getaffinity(0))))
+    d = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.TemporaryDirectory(dir=d) as tmp:
+        npz = os.path.join(tmp, "c3.npz")
+        np.savez(npz, **arrs)
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(w, initializer=_pool_init, initargs=(npz, reference_dir())) as pool:
+            pool.map(_pool_corner, range(w), chunksize=1)          # warm-up: every worker once
+            t0 = time.perf_counter()
+            pool.map(_pool_corner, range(n_total), chunksize=1)
+            dt = time.perf_counter() - t0
+    kind = "reference" if reference_dir() else "port"
+    return {"value": round(n_total / dt, 3), "unit": "corners/s", "cores": w, "kind": kind,
+            "sample": f"all {n_total} C5 corners of C3 (run_engine + timing_gradients each) over a "
+                      f"spawn pool of {w} workers after a warm-up map; {cpu_model()}"}
+
+
+def cpu_placement(raw, n_inv=2, sigma_um=0.5, seed=1000):
+    """C4 on the host (the oracle port: the reference has no position model):
+    wire RC -> run_engine -> timing_gradients -> position gradients for
+    n_inv invocations, one core."""
+    from oracle import oracle as O
+    from paper_2603_28381_b200 import placement as PL
+    pl = PL.synthetic_placement(raw, seed=3)
+    flat = O.flatten_raw(raw)
+    rng = np.random.default_rng(seed)
+    xys = [pl.xy + sigma_um * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin] for _ in range(n_inv)]
+    it = iter(range(10 ** 9))
+
+    def one():
+        xy = xys[next(it) % n_inv]
+        res, cap = O.wire(flat, xy, pl.res0, pl.cap0, pl.wire.r_unit, pl.wire.c_unit)
+        f = O.with_values(flat, mem_res=res, mem_cap=cap)
+        st = O.run_engine(f)
+        gr = O.timing_gradients(f, st)
+        O.position_gradients(f, st, gr, xy, pl.wire.r_unit, pl.wire.c_unit)
+    r = time_cpu(one, n_inv, 30.0)
+    return {"value": round(r["ms"], 3), "unit": "ms per invocation", "cores": 1, "kind": "port",
+            "sample": f"{r['runs']} C4 invocations after 1 warm-up (oracle/sta_oracle.c: wire RC, "
+                      f"run_engine, timing_gradients, position gradients; the reference has no "
+                      f"position model), core {r['core']}; {cpu_model()}"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# GPU workloads
+
+def device_median(fn, steps, flush, stream):
+    """Median device time of fn() over `steps` runs, CUDA events on `stream`,
+    the >L2 flush buffer rewritten before each run (outside the events)."""
+    import torch
+    ts = []
+    for i in range(steps):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), ts
+
+
+def corner_batch(raw, rank, world, steps, flush, dist=None, n_total=16):
     """C5: 16 corners of the C3 netlist sharded round-robin
     over the ranks (corner k -> rank k mod world, 16/world per GPU), all of a
-    rank's corners in ONE ws_run (blockIdx.y = corner), then the batch
-    objective's NCCL exchange: TNS / loss SUM, WNS MIN, d_arc / d_edge SUM
-    (the gradient of sum_k loss_k).  Device time with CUDA events, max over
-    ranks; corners/s is the whole job's."""
+    rank's corners in ONE ws_run (blockIdx.y = corner) that also writes the
+    batch gradient sum_k d_arc / sum_k d_edge (WS_RUN_CORNER_SUM); then the
+    batch objective's exchange — TNS / loss SUM, WNS MIN, the gradient sums
+    SUM — on a side stream, overlapped with the next batch (two reduce
+    buffers).  Device time with CUDA events, max over ranks; corners/s is the
+    whole job's."""
     import torch
     import paper_2603_28381_b200 as ws
-    from paper_2603_28381_b200.corners import combine_local, reduce_batch
-    mine = [k for k in range(n_total) if k % world == rank]
+    from paper_2603_28381_b200 import _lib
+    from paper_2603_28381_b200.corners import combine_local, corners_of_rank, reduce_batch
+    mine = corners_of_rank(n_total, rank, world)
     nc = len(mine)
     dev = ws.DeviceDesign(raw, n_corners=nc)
     for i, k in enumerate(mine):
         dev.set_values(i, **corner_values(raw, k))
+    flags = (_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED | _lib.RUN_GRAPH |
+             _lib.RUN_CORNER_SUM)
     stream = torch.cuda.current_stream()
-    d_arc = [dev.tensor("d_arc", i) for i in range(nc)]
-    d_edge = [dev.tensor("d_edge", i) for i in range(nc)]
+    side = torch.cuda.Stream()
     summ = [dev.tensor("summary", i) for i in range(nc)]
-    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+    dsum = (dev.tensor("d_arc_sum"), dev.tensor("d_edge_sum"))
+    red = [(torch.empty_like(dsum[0]), torch.empty_like(dsum[1]), torch.empty(3, dtype=torch.float64,
+                                                                                device="cuda"))
+           for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
 
-    def step():
+    def step(i):
+        b = i % 2
+        stream.wait_event(done[b])                 # reduce buffer b free again
         dev.run(flags, corner=0, n_corners=nc, stream=stream)
-        ga, ge = d_arc[0].clone(), d_edge[0].clone()
-        for i in range(1, nc):
-            ga += d_arc[i]
-            ge += d_edge[i]
-        sm = combine_local(summ)
+        ra, re, rs = red[b]
+        ra.copy_(dsum[0])
+        re.copy_(dsum[1])
+        rs.copy_(combine_local(summ))
+        ready[b].record(stream)
         if dist is not None:
-            reduce_batch(sm, ga, ge)
-        return sm
+            with torch.cuda.stream(side):
+                side.wait_event(ready[b])
+                reduce_batch(rs, ra, re)
+                done[b].record(side)
+        else:
+            done[b].record(stream)
 
-    for _ in range(3):
-        step()
+    for i in range(3):
+        step(i)
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
+    launches = dev.last_launch_count()
     if dist is not None:
         dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.fill_(0)
+    e0.record(stream)
     for i in range(steps):
-        flush.fill_(i)
-        evs[i][0].record(stream)
-        sm = step()
-        evs[i][1].record(stream)
+        step(i)
+    stream.wait_stream(side)                       # the last exchange is inside the region
+    e1.record(stream)
     torch.cuda.synchronize()
-    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = float(tot.item()) / steps
-    out = {"workload": "C5: %d corners of the C3 netlist, corner k -> rank k mod N, a rank's "
-                       "corners in one ws_run, NCCL TNS/loss SUM, WNS MIN, d_arc/d_edge SUM" % n_total,
+    res = red[(steps - 1) % 2][2]
+    out = {"workload": "C5: %d corners of the C3 netlist, corner k -> rank k mod N, a rank's corners "
+                       "in one ws_run with the in-kernel batch gradient sum, then NCCL TNS/loss SUM, "
+                       "WNS MIN, gradient SUM on a side stream overlapped with the next batch" % n_total,
            "corners_per_gpu": nc, "ms_per_batch": round(ms, 4),
            "corners_per_s": round(n_total / (ms * 1e-3), 2), "steps": steps,
-           "batch_result": {"tns": float(sm[0]), "wns": float(sm[1]), "loss": float(sm[2])}}
+           "gpu_launches_per_batch": launches,
+           "achieved_gbs": round(n_total * C3_BYTES / (ms * 1e-3) / 1e9, 1),
+           "batch_result": {"tns": float(res[0]), "wns": float(res[1]), "loss": float(res[2])}}
     dev.close()
     return out
 
@@ -255,22 +444,21 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
         dev.run(flags, corner=0, n_corners=nc, gamma=timers[0].gamma, stream=stream)
         s = torch.stack(summ)
         if dist is not None:
-            return gather_candidates(s, torch.stack(dxy))
+            return gather_candidates(s, torch.stack(dxy), n_candidates=n_total)
         return s, torch.stack(dxy)
 
     for _ in range(5):                       # first calls in a process are slower
         step()
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
     if dist is not None:
         dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
     for i in range(steps):
-        evs[i][0].record(stream)
         s, _ = step()
-        evs[i][1].record(stream)
+    e1.record(stream)
     torch.cuda.synchronize()
-    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = float(tot.item()) / steps
@@ -285,31 +473,22 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
     return out
 
 
-def c2_sta(steps=20):
+def c2_sta(flush, steps=20, cpu=True):
     """C2: the ICCAD-2015-shaped 995,808-pin heavy-tail
     netlist, forward AT / RAT / slack + TNS/WNS only (run_engine), one B200;
-    CUDA events per pass, a >L2 buffer rewritten between passes.  Roofline
-    on B_sta."""
+    median of CUDA-event-timed passes, a >L2 buffer rewritten between passes.
+    Roofline on B_sta; the reference's run_engine on the
+    same netlist as its CPU baseline."""
     import torch
     import paper_2603_28381_b200 as ws
     from paper_2603_28381_b200 import _lib, generator as G
     raw = G.generate_raw(G.config_c2())
     dev = ws.DeviceDesign(raw)
     flags = _lib.RUN_HARD | _lib.RUN_GRAPH
-    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
     for _ in range(3):
         dev.run(flags, stream=stream)
-    ts = []
-    for i in range(steps):
-        flush.fill_(i)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        dev.run(flags, stream=stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = statistics.median(ts)
+    ms, _ = device_median(lambda: dev.run(flags, stream=stream), steps, flush, stream)
     P, M, N, A, I, E = dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep
     B = 224 * P + 76 * M + 44 * N + 76 * A + 68 * I + 36 * E
     peak, _ = measured_peaks()
@@ -320,6 +499,11 @@ def c2_sta(steps=20):
            "achieved_gbs": round(B / (ms * 1e-3) / 1e9, 1), "frac": round(B / (ms * 1e-3) / 1e9 / peak, 4),
            "launches": dev.last_launch_count(), "tns": tns, "wns": wns}
     dev.close()
+    if cpu:
+        r = time_reference(raw, max_passes=3, budget_s=20.0, hard_only=True)
+        out["cpu_baseline"] = {"value": round(r["ms"], 3), "unit": "ms", "cores": 1, "kind": r["kind"],
+                               "sample": f"{r['runs']} C2 run_engine passes after 1 warm-up "
+                                         f"({r['what']}), core {r['core']}; {cpu_model()}"}
     return out
 
 
@@ -334,7 +518,8 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     adjoint -> position gradients.  Device time: CUDA events around all
     n_inv invocations (each = D2D install of its coordinates + ws_run).  e2e:
     the same loop through the public API with each invocation's positions
-    copied from pinned host memory and loss / TNS / WNS read back."""
+    copied from pinned host memory, and dL/dxy plus loss / TNS / WNS copied
+    back to pinned host memory, every invocation."""
     import torch
     import paper_2603_28381_b200 as ws
     from paper_2603_28381_b200 import placement as PL
@@ -347,7 +532,6 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     cop = torch.as_tensor(pl.cell_of_pin, device="cuda")
     off = torch.as_tensor(pl.pin_offset, device="cuda")
     xy = dev.value_tensor("xy")          # the corner's position array in HBM
-    summ = dev.tensor("summary")
     # every invocation's coordinates, generated on the device up front (the
     # placer's input stream; 8 GB of HBM at C3): cell k of invocation t moves
     # by N(0, sigma) from torch's Philox stream seeded seed + t
@@ -376,17 +560,23 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     loss_last = dev.summary()
     # e2e: positions from pinned host memory (copy stream, straight into one
     # of two corner slots so invocation t+1's copy overlaps invocation t),
-    # summary back, every invocation
+    # dL/dxy and the summary back to pinned host memory on a second copy
+    # stream, every invocation
     rng = np.random.default_rng(seed)
     host_xy = [torch.from_numpy(np.ascontiguousarray(
         pl.xy + sigma_um * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin])).pin_memory()
         for _ in range(2)]
-    h_out = torch.zeros(3, dtype=torch.float64).pin_memory()
+    h_out = [torch.zeros(3, dtype=torch.float64).pin_memory() for _ in range(2)]
+    h_dxy = [torch.empty(tuple(dev.tensor("d_xy", b).shape), dtype=torch.float64).pin_memory()
+             for b in range(2)]
     xys = [dev.value_tensor("xy", b) for b in range(2)]
     summs = [dev.tensor("summary", b) for b in range(2)]
-    cstream = torch.cuda.Stream()
+    dxys = [dev.tensor("d_xy", b) for b in range(2)]
+    cstream, ostream = torch.cuda.Stream(), torch.cuda.Stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
+    ran = [torch.cuda.Event() for _ in range(2)]
+    out_done = [torch.cuda.Event() for _ in range(2)]
 
     def copy_in(t):
         b = t % 2
@@ -398,14 +588,21 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     def e2e_inv(t, nxt=True):
         b = t % 2
         stream.wait_event(copied[b])
+        stream.wait_event(out_done[b])           # slot b's previous results are out
         if nxt:
             copy_in(t + 1)
         dev.run(timer.flags, corner=b, gamma=timer.gamma, stream=stream)
         consumed[b].record(stream)
-        h_out.copy_(summs[b], non_blocking=True)
+        ran[b].record(stream)
+        ostream.wait_event(ran[b])
+        with torch.cuda.stream(ostream):
+            h_dxy[b].copy_(dxys[b], non_blocking=True)
+            h_out[b].copy_(summs[b], non_blocking=True)
+        out_done[b].record(ostream)
 
     for b in range(2):
         consumed[b].record(stream)
+        out_done[b].record(stream)
     copy_in(0)
     e2e_inv(0)
     e2e_inv(1, nxt=False)
@@ -416,6 +613,7 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
     copy_in(0)
     for t in range(n_e2e):
         e2e_inv(t, nxt=t + 1 < n_e2e)
+    stream.wait_stream(ostream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / n_e2e
@@ -427,21 +625,96 @@ def placement_loop(raw, n_inv=200, sigma_um=0.5, seed=1000):
             "ms_per_invocation": round(dev_ms / n_inv, 4),
             "launches_per_invocation": launches,
             "e2e": {"ms_per_invocation": round(e2e_ms, 4), "invocations": n_e2e,
-                    "h2d_bytes_per_step": int(host_xy[0].numel() * 8), "d2h_bytes_per_step": 24},
+                    "h2d_bytes_per_step": int(host_xy[0].numel() * 8),
+                    "d2h_bytes_per_step": int(h_dxy[0].numel() * 8 + 24)},
             "last": {"tns": loss_last[0], "wns": loss_last[1], "loss": loss_last[2]}}
 
 
-def cpu_model():
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return "unknown"
+def e2e_dropin(raw, reps=5):
+    """The reference's plugin call through this package's drop-in API:
+    ``st = run_engine(flat)`` then ``timing_gradients(flat, state=st)``
+    (warp.py:462-476, diff.py:266-273), numpy arrays in and out — the value
+    arrays uploaded, the TimingState and GradientState downloaded, every
+    call.  Host wall time (the calls are synchronous), median of `reps`."""
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200.warp import run_engine
+    flat = ws.flatten(raw)
+    vals = ("mem_res", "mem_cap", "root_cap", "lut_t_flat", "pi_arrival", "pi_slew", "ep_required")
+
+    def call():
+        st = run_engine(flat)
+        gs = ws.timing_gradients(flat, state=st)
+        return st, gs
+
+    st, gs = call()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        st, gs = call()
+        ts.append(time.perf_counter() - t0)
+    vb = sum(getattr(flat, v).nbytes for v in vals)
+    h2d = 2 * vb + st.arrival.nbytes + st.net_delay.nbytes + st.arc_delay.nbytes
+    d2h = (sum(getattr(st, f).nbytes for f in ("load", "net_delay", "impulse", "slew", "arrival",
+                                                 "required", "slack", "arc_delay")) +
+           sum(getattr(gs, f).nbytes for f in ("lse_arrival", "arc_weights", "d_arc", "d_edge",
+                                                "adjoint")))
+    flat.dev.close()
+    return {"value": round(1e3 * statistics.median(ts), 3), "unit": "ms", "reps": reps,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "how": "run_engine(flat) + timing_gradients(flat, state=st) on the C3 FlatDesign: "
+                   "value arrays up, TimingState + GradientState down as numpy (pinned), host wall "
+                   "clock, median",
+            "times_ms": [round(1e3 * t, 2) for t in ts]}
+
+
+def inpass_classes():
+    """Per-kernel-class in-pass time of the fused C3 pass (profiles/
+    inpass_r02.json: globaltimer stamps of every block of one graph-replayed
+    pass, WS_PROBE build; a launch's share is the critical-path increment from
+    the previous launch's last block to its own, so the classes add up to the
+    pass) and the per-pass DRAM traffic of the whole pass (profiles/
+    traffic_r02.json: ncu range replay over one graph launch)."""
+    out = {}
+    for name, key in (("inpass_r02.json", "classes"), ("traffic_r02.json", "traffic")):
+        p = os.path.join(REPO, "profiles", name)
+        if os.path.exists(p):
+            try:
+                out[key] = json.load(open(p))
+            except Exception:
+                pass
+    return out
 
 
 # ---------------------------------------------------------------------------
+
+C3_BYTES = 1034449488       # SURVEY.md §8(d) B_fwdbwd(C3)
+
+
+def reference_arm(args, rank, config):
+    if rank != 0:
+        return 0
+    from paper_2603_28381_b200 import generator as G
+    t0 = time.time()
+    cfg = {"c1": G.config_c1(), "c2": G.config_c2(), "c3": G.config_c3()}[args.workload]
+    raw = G.generate_raw(cfg)
+    log(f"[ref] generated {raw.n_pins} pins in {time.time() - t0:.1f}s")
+    budget = max(30.0, min(150.0, 6.0 * (args.steps + args.warmup)))
+    r = time_reference(raw, max_passes=args.steps, budget_s=budget)
+    line = {"impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
+            "n_gpus": args.gpus, "steps": r["runs"], "warmup": 1,
+            "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
+            "config": config,
+            "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": 1, "kind": r["kind"],
+                             "sample": f"median of {r['runs']} full {args.workload.upper()} passes "
+                                       f"(run_engine + timing_gradients) after 1 warm-up "
+                                       f"({r['what']}), pinned to core {r['core']} with one BLAS/OpenMP "
+                                       f"thread (single-threaded by construction); {cpu_model()}"},
+            "e2e": {"value": round(r["ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -458,6 +731,7 @@ def main():
                     help="also measure the C5 16-corner batch (corner_batch key); 0: skip")
     ap.add_argument("--placement", type=int, default=200,
                     help="C4 placement-loop invocations reported under placement_loop (0: skip)")
+    ap.add_argument("--dropin", type=int, default=1, help="measure e2e_dropin (0: skip)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -473,29 +747,10 @@ def main():
               "parallelism": f"corner-sharded x{args.gpus} (weak)"}
 
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        t0 = time.time()
-        raw = G.generate_raw(cfg)
-        log(f"[ref] generated {raw.n_pins} pins in {time.time() - t0:.1f}s")
-        budget = max(30.0, min(150.0, 6.0 * (args.steps + args.warmup)))
-        r = time_reference(raw, max_passes=args.steps, budget_s=budget)
-        cores = 1
-        line = {"impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
-                "n_gpus": args.gpus, "steps": r["passes"], "warmup": 1,
-                "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
-                "config": config,
-                "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": cores,
-                                 "kind": r["kind"],
-                                 "sample": f"{r['passes']} full C3 passes after 1 warm-up "
-                                           f"({r['what']}, single-threaded by construction, "
-                                           f"{cpu_model()})"},
-                "e2e": {"value": round(r["ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args, rank, config)
 
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator lines for the driver's rank check
     import torch
     # WS_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo, so
     # the N>1 path can be exercised on a one-GPU box
@@ -521,7 +776,7 @@ def main():
     raw = G.generate_raw(cfg)
     t_gen = time.time() - t0
     t0 = time.time()
-    dev = ws.DeviceDesign(raw, n_corners=2)     # corner 1: the e2e's second input slot
+    dev = ws.DeviceDesign(raw, n_corners=2)     # two slots: pass i runs slot i % 2
     torch.cuda.synchronize()
     t_build = time.time() - t0
     if world > 1 or rank > 0:
@@ -536,70 +791,86 @@ def main():
     if args.graph:
         flags |= _lib.RUN_GRAPH
     stream = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
 
-    # zero-copy torch views of the corner's results in HBM
-    d_arc, d_edge, summ = dev.tensor("d_arc"), dev.tensor("d_edge"), dev.tensor("summary")
+    # zero-copy torch views of each slot's results in HBM
+    grads = [(dev.tensor("d_arc", b), dev.tensor("d_edge", b)) for b in range(2)]
+    summs = [dev.tensor("summary", b) for b in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    reduced = [torch.cuda.Event() for _ in range(2)]
+    for b in range(2):
+        reduced[b].record(stream)
 
-    def step():
-        dev.run(flags, stream=stream)
-
-    def collectives():
+    def step(i):
+        b = i % 2
+        stream.wait_event(reduced[b])        # slot b's previous exchange has read it
+        dev.run(flags, corner=b, stream=stream)
         if world > 1:
-            # the batch objective: TNS / loss SUM, WNS MIN, gradients SUM
-            reduce_batch(summ, d_arc, d_edge)
+            # the batch objective (TNS / loss SUM, WNS MIN, gradients SUM,
+            # SURVEY §8(e)) on the side stream, overlapped with pass i+1
+            ready[b].record(stream)
+            with torch.cuda.stream(side):
+                side.wait_event(ready[b])
+                reduce_batch(summs[b], *grads[b])
+                reduced[b].record(side)
+        else:
+            reduced[b].record(stream)
 
-    for _ in range(max(3, args.warmup)):
-        step()
-        collectives()
+    for i in range(max(3, args.warmup)):
+        step(i)
     torch.cuda.synchronize()
     launches = dev.last_launch_count()
 
     # ---- timed region: K passes, each bracketed by CUDA events on the launch
-    # stream; a >L2 buffer is rewritten between passes (outside the events)
+    # stream; a >L2 buffer is rewritten between passes (outside the events);
+    # the whole region (with the last exchange) is bracketed too
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        g0.record(stream)
         for i in range(args.steps):
             flush.fill_(i)
             evs[i][0].record(stream)
-            step()
-            collectives()
+            step(i)
             evs[i][1].record(stream)
+        stream.wait_stream(side)
+        g1.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     per = [a.elapsed_time(b) for a, b in evs]
-    tot = torch.tensor([sum(per)], dtype=torch.float64, device="cuda")
+    med = statistics.median(per)
+    tot = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms_step = float(tot.item()) / args.steps
+    ms_step = med if world == 1 else float(tot.item()) / args.steps
     value = ms_step / world
-    tns, wns, loss = dev.summary()
+    tns, wns, loss = dev.summary((args.steps - 1) % 2)
 
-    # ---- e2e through the public API with pinned host inputs
+    # ---- e2e through the public API with pinned host buffers: each step's
+    # RC inputs H2D straight into one of the two slots (copy stream, so step
+    # i+1's copy overlaps step i's pass), the pass, then the step's gradients
+    # d_arc / d_edge and TNS/WNS/loss D2H on a second copy stream (overlapping
+    # the next pass).  Every step's H2D and D2H is inside the timed region.
     vals = corner_values(raw, rank) if (world > 1 or rank > 0) else dict(
         mem_res=raw.mem_res, mem_cap=raw.mem_cap, root_cap=raw.root_cap)
     h_in = {k: torch.from_numpy(np.ascontiguousarray(vals[k])).pin_memory()
             for k in ("mem_res", "mem_cap", "root_cap")}
-    h_out = torch.zeros(3, dtype=torch.float64).pin_memory()
+    h_out = [{"d_arc": torch.empty(tuple(grads[b][0].shape), dtype=torch.float64).pin_memory(),
+              "d_edge": torch.empty(tuple(grads[b][1].shape), dtype=torch.float64).pin_memory(),
+              "summary": torch.zeros(3, dtype=torch.float64).pin_memory()} for b in range(2)]
     h2d = sum(t.numel() for t in h_in.values()) * 8
-    d2h = h_out.numel() * 8
-
-    # Each step's RC inputs go H2D straight into one of two corner slots of
-    # the context (corner i % 2; both share the topology), so step i+1's copy
-    # overlaps step i's pass and no device-to-device install competes with
-    # the copy engine.  The step then runs its slot and reads TNS / WNS / loss
-    # back.  Every step's H2D and D2H is inside the timed region.
-    cstream = torch.cuda.Stream()
+    d2h = sum(t.numel() for t in h_out[0].values()) * 8
+    cstream, ostream = torch.cuda.Stream(), torch.cuda.Stream()
     views = [{k: dev.value_tensor(k, b) for k in h_in} for b in range(2)]
-    summs = [dev.tensor("summary", b) for b in range(2)]
-    grads = [(dev.tensor("d_arc", b), dev.tensor("d_edge", b)) for b in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
+    out_done = [torch.cuda.Event() for _ in range(2)]
 
     def stage_copy(i):
         b = i % 2
@@ -612,16 +883,23 @@ def main():
     def e2e_step(i, prefetch_next=True):
         b = i % 2
         stream.wait_event(copied[b])
+        stream.wait_event(out_done[b])           # slot b's previous results are out
         if prefetch_next:
             stage_copy(i + 1)
         dev.run(flags, corner=b, stream=stream)
-        consumed[b].record(stream)
         if world > 1:
             reduce_batch(summs[b], *grads[b])
-        h_out.copy_(summs[b], non_blocking=True)
+        consumed[b].record(stream)
+        ostream.wait_event(consumed[b])
+        with torch.cuda.stream(ostream):
+            h_out[b]["d_arc"].copy_(grads[b][0], non_blocking=True)
+            h_out[b]["d_edge"].copy_(grads[b][1], non_blocking=True)
+            h_out[b]["summary"].copy_(summs[b], non_blocking=True)
+        out_done[b].record(ostream)
 
     for b in range(2):
         consumed[b].record(stream)
+        out_done[b].record(stream)
     stage_copy(0)
     e2e_step(0)
     e2e_step(1, prefetch_next=False)
@@ -640,6 +918,7 @@ def main():
         stage_copy(0)                        # the first timed step's inputs
         for i in range(ke):
             e2e_step(i, prefetch_next=i + 1 < ke)
+        stream.wait_stream(ostream)
         e1.record(stream)
         torch.cuda.synchronize()
         windows.append(e0.elapsed_time(e1))
@@ -647,66 +926,21 @@ def main():
     if dist:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / ke / world
-
-    # per-kernel-class breakdown of the same pass: a fused pass with a CUDA
-    # event after every launch (the events serialise the PDL overlap, so the
-    # classes sum to more than the pass), and the ncu-measured DRAM bytes of
-    # each class (profiles/traffic_*.json) over its event time
-    kclass = None
-    if rank == 0:
-        tflags = (flags & ~_lib.RUN_GRAPH) | _lib.RUN_TIMED
-        runs = []
-        for _ in range(4):
-            dev.run(tflags, stream=stream)
-            runs.append(dev.kernel_times())
-        names = {0: "k_rc_flat (+free pins)", 1: "k_fwd<1,1> (fwd+LSE level)",
-                 2: "k_bwd<1,1> (bwd+grad level)", 5: "k_fin_summary"}
-        acc = {}
-        for kt in runs[1:]:
-            for kind, lvl, ms in kt:
-                a = acc.setdefault(kind, [0, 0.0])
-                a[0] += 1
-                a[1] += ms
-        traffic_pk = {}
-        tp = os.path.join(REPO, "profiles", "traffic_r01.json")
-        if os.path.exists(tp):
-            try:
-                for k, v in json.load(open(tp)).get("per_kernel", {}).items():
-                    for key, nm in (("k_rc_flat", 0), ("k_fwd<", 1), ("k_bwd<", 2), ("k_fin_summary", 5)):
-                        if key in k:
-                            traffic_pk[nm] = v["dram_bytes"] / max(1, v["launches"])
-            except Exception:
-                traffic_pk = {}
-        kclass = []
-        for kind in (1, 2, 0, 5):
-            if kind not in acc:
-                continue
-            n, tot = acc[kind]
-            avg_us = 1e3 * tot / n
-            row = {"kernel": names[kind], "launches_per_pass": n // (len(runs) - 1),
-                   "avg_launch_us": round(avg_us, 2)}
-            if kind in traffic_pk:
-                row["dram_bytes_per_launch"] = int(traffic_pk[kind])
-                row["dram_gbs"] = round(traffic_pk[kind] / (avg_us * 1e-6) / 1e9, 1)
-            kclass.append(row)
+    dev.close()
 
     cb = pb = None
     if args.corners and 16 % world == 0:
-        cb = corner_batch(raw, rank, world, flags, steps=max(3, min(args.steps, 10)), dist=dist)
+        cb = corner_batch(raw, rank, world, steps=max(3, min(args.steps, 10)), flush=flush, dist=dist)
         pb = candidate_batch(raw, rank, world, steps=6, dist=dist)
 
     if rank == 0:
-        P, M, N, A, I, E = (dev.n_pins, dev.n_members, dev.n_nets, dev.n_arcs, dev.n_pi, dev.n_ep)
+        P, M, N, A, I, E = (raw.n_pins, raw.n_members, raw.n_nets, raw.n_arcs, len(raw.pi_pin),
+                            len(raw.ep_pin))
         B = algorithmic_bytes(P, M, N, A, I, E)
         peak, peak_src = measured_peaks()
         achieved = B / (ms_step * 1e-3) / 1e9
-        traffic = None
-        tp = os.path.join(REPO, "profiles", "traffic_r01.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get("bytes_per_pass")
-            except Exception:
-                traffic = None
+        prof = inpass_classes()
+        traffic = prof.get("traffic", {}).get("bytes_per_pass")
         line = {"metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -714,6 +948,10 @@ def main():
                 "config": dict(config, mode=args.mode, cuda_graph=bool(args.graph),
                                l2="inputs larger than L2 (1.03 GB/pass vs 126 MB) and a 252 MB "
                                   "buffer rewritten between timed passes"),
+                "timing": ("median of %d CUDA-event-timed passes" % args.steps if world == 1 else
+                           "max over ranks of the K-step region (passes + overlapped exchanges) / K"),
+                "step_ms": {"median": round(med, 4), "min": round(min(per), 4), "max": round(max(per), 4),
+                            "mean": round(sum(per) / len(per), 4)},
                 "corners_per_s": round(1e3 / value, 2),
                 "achieved_hbm_gbs": round(achieved, 1),
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -722,16 +960,22 @@ def main():
                              "algorithmic_bytes_per_pass": B, "peak_source": peak_src},
                 "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h,
-                        "how": "public API (DeviceDesign value_tensor views / run / summary view): "
+                        "how": "public API (DeviceDesign value_tensor views / run / result views): "
                                "each step's pinned H2D on a copy stream straight into one of two "
                                "corner slots, so step i+1's copy overlaps step i's pass; D2H of "
-                               "TNS/WNS/loss every step"},
+                               "d_arc, d_edge and TNS/WNS/loss into pinned memory on a second copy "
+                               "stream every step"},
                 "gpu_launches": launches * args.steps,
                 "clocks": clk.summary(),
                 "result": {"tns": tns, "wns": wns, "loss": loss},
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
-        if kclass:
-            line["roofline"]["kernel_classes"] = kclass
+        if "classes" in prof:
+            line["roofline"]["kernel_classes"] = prof["classes"].get("classes")
+            line["roofline"]["kernel_classes_source"] = prof["classes"].get("what")
+        if "traffic" in prof:
+            line["roofline"]["traffic_source"] = prof["traffic"].get("what")
+        if world == 1 and args.dropin:
+            line["e2e_dropin"] = e2e_dropin(raw)
         if cb is not None:
             line["corner_batch"] = cb
         if pb is not None:
@@ -739,17 +983,22 @@ def main():
         if args.placement and world == 1:
             line["placement_loop"] = placement_loop(raw, n_inv=args.placement)
         if args.corners and world == 1:
-            line["c2_sta"] = c2_sta()
+            line["c2_sta"] = c2_sta(flush, cpu=bool(args.cpu_baseline))
         if args.cpu_baseline and world == 1:
             r = time_reference(raw, max_passes=3, budget_s=25.0)
             line["cpu_baseline"] = {"value": round(r["ms"], 3), "unit": "ms", "cores": 1,
                                     "kind": r["kind"],
-                                    "sample": f"{r['passes']} full C3 passes after 1 warm-up "
-                                              f"({r['what']}; {cpu_model()})"}
+                                    "sample": f"median of {r['runs']} full C3 passes (run_engine + "
+                                              f"timing_gradients) after 1 warm-up ({r['what']}), "
+                                              f"pinned to core {r['core']}, one BLAS/OpenMP thread; "
+                                              f"{cpu_model()}"}
+            if args.placement:
+                line["placement_loop"]["cpu_baseline"] = cpu_placement(raw)
+            if cb is not None:
+                line["corner_batch"]["cpu_baseline"] = cpu_corner_pool(raw)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-    dev.close()
     return 0
 
 

@@ -84,8 +84,7 @@ class GradientState:
 
     @classmethod
     def from_device(cls, dev, corner, gamma, loss_kind, flat=None):
-        g = cls(gamma=gamma, loss_kind=loss_kind,
-                **{f: dev.get(f, corner) for f in GRAD_FIELDS}, flat=flat)
+        g = cls(gamma=gamma, loss_kind=loss_kind, **dev.get_many(GRAD_FIELDS, corner), flat=flat)
         g.loss = dev.summary(corner)[2]
         return g
 

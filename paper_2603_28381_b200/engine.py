@@ -235,6 +235,23 @@ class DeviceDesign:
                                _stream_handle(stream)))
         return out
 
+    def get_many(self, names, corner: int = 0) -> dict:
+        """Several result arrays of one corner as numpy arrays in PINNED host
+        memory: all device-to-host copies are queued on the current stream
+        back to back (full copy-engine bandwidth, no pageable staging) and
+        synchronised once.  The buffers come from torch's caching host
+        allocator, so repeated calls reuse them."""
+        import torch
+        host = {}
+        for n in names:
+            src = self.tensor(n, corner)
+            h = torch.empty(tuple(src.shape), dtype=torch.float64, pin_memory=True)
+            if h.numel():
+                h.copy_(src, non_blocking=True)
+            host[n] = h
+        torch.cuda.current_stream().synchronize()
+        return {n: h.numpy() for n, h in host.items()}
+
     def set_state(self, corner: int = 0, stream=None, **arrays):
         """Overwrite result arrays of one corner (host numpy arrays)."""
         L = lib()

@@ -55,7 +55,7 @@ class TimingState:
 
     @classmethod
     def from_device(cls, dev, corner: int = 0, n_levels: int = 0) -> "TimingState":
-        return cls(**{f: dev.get(f, corner) for f in STATE_FIELDS}, n_levels=n_levels)
+        return cls(**dev.get_many(STATE_FIELDS, corner), n_levels=n_levels)
 
     def values_equal(self, other: "TimingState", rtol=1e-6, atol=1e-22) -> bool:
         return all(
