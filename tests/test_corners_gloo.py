@@ -128,3 +128,55 @@ def test_gloo_world2_candidate_gather_uneven(tmp_path):
     assert got["s"][:, 0].tolist() == [-float(c) for c in range(5)]
     assert all(float(got["g"][c, 0, 0]) == float(c) for c in range(5))
     assert got["best"] == 4
+
+
+def _engine_worker(rank, world, port, name, out):
+    """One rank on the shared cuda:0: its round-robin corners of the design
+    in ONE batched ws_run (with the in-kernel batch gradient sum), then the
+    batch exchange over gloo."""
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    import paper_2603_28381_b200 as ws
+    from paper_2603_28381_b200 import _lib
+    from golden_util import load, raw_of
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        raw = raw_of(load(name))
+        mine = CO.corners_of_rank(N_CORNERS, rank, world)
+        dev = ws.DeviceDesign(raw, n_corners=len(mine))
+        for i, k in enumerate(mine):
+            dev.set_values(i, **CO.corner_values(raw, k))
+        dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED | _lib.RUN_CORNER_SUM,
+                corner=0, n_corners=len(mine), gamma=0.01 * raw.clock_period)
+        summ = CO.combine_local([dev.tensor("summary", i) for i in range(len(mine))]).cpu()
+        d_arc = dev.tensor("d_arc_sum").cpu()
+        d_edge = dev.tensor("d_edge_sum").cpu()
+        CO.reduce_batch(summ, d_arc, d_edge)
+        if rank == 0:
+            torch.save({"summ": summ, "d_arc": d_arc, "d_edge": d_edge}, out)
+        dev.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gen_c1_star", "multi_out"])
+def test_gloo_world2_engine_batch_on_shared_gpu(tmp_path, name):
+    """The multi-GPU data plane with real engine outputs: 2 ranks sharing
+    cuda:0, each running its corners through the C-ABI, reduced over gloo;
+    rank 0's batch TNS / WNS / loss and gradient sums against the oracle's
+    serial evaluation of all 4 corners."""
+    out = str(tmp_path / "e0.pt")
+    mp.spawn(_engine_worker, args=(2, _free_port(), name, out), nprocs=2, join=True)
+    got = torch.load(out)
+    ref = [_corner_result(name, k) for k in range(N_CORNERS)]
+    exp = CO.combine_local([r[0] for r in ref])
+    assert float(got["summ"][1]) == float(exp[1])
+    np.testing.assert_allclose(got["summ"][[0, 2]].numpy(), exp[[0, 2]].numpy(), rtol=1e-9)
+    for key, idx in (("d_arc", 1), ("d_edge", 2)):
+        e = sum(r[idx] for r in ref).numpy()
+        scale = max(float(np.abs(e).max()), 1e-300)
+        np.testing.assert_allclose(got[key].numpy(), e, rtol=1e-4, atol=1e-9 * scale)
