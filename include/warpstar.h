@@ -167,6 +167,15 @@ int ws_perturb_values(ws_ctx *ctx, int corner, int base_corner, uint64_t seed, d
 int ws_run(ws_ctx *ctx, int corner0, int n_corners, uint32_t flags, double gamma,
            int loss_kind, int reduce_width, int granularity, void *stream, void *stream_grad);
 
+/* One kernel of the fusion pipeline's graph (fusion.py:113-160), launched
+ * alone on `stream`: kind 0 net_rc, 1 cell_delay_at, 2 slack_bwd, 3 lse_fwd,
+ * 4 grad_bwd at `level`; 5 finish (free-pin / PI-root adjoints, TNS / WNS /
+ * loss; level ignored).  The caller owns the ordering — the Python
+ * PipelineRun checks each kernel's dependencies before launching it and
+ * raises FusionError on a violation (replaces fusion.py:307-312). */
+int ws_run_kernel(ws_ctx *ctx, int corner, int kind, int level, double gamma, int loss_kind,
+                  int reduce_width, void *stream);
+
 /* Overwrite a result array of one corner (e.g. a caller-supplied TimingState
  * handed to forward_lse_arrival). */
 int ws_set_state(ws_ctx *ctx, int corner, int field, const double *src, int src_on_device,

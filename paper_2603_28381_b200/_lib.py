@@ -58,7 +58,7 @@ EXPORTS = ("ws_abi_version", "ws_last_error", "ws_last_error_pin", "ws_create", 
            "ws_dims", "ws_topology_len", "ws_get_topology", "ws_set_values",
            "ws_perturb_values", "ws_run", "ws_get", "ws_device_ptr", "ws_value_ptr",
            "ws_summary", "ws_last_launch_count", "ws_set_state", "ws_set_probe", "ws_rc_level", "ws_forward_level",
-           "ws_backward_level", "ws_kernel_times")
+           "ws_backward_level", "ws_kernel_times", "ws_run_kernel")
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_i32p = ctypes.POINTER(ctypes.c_int32)
@@ -119,6 +119,8 @@ def lib():
                                     ctypes.c_double, _vp]
     L.ws_run.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_double,
                          ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    L.ws_run_kernel.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_int, ctypes.c_int, _vp]
     L.ws_get.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]
     L.ws_set_state.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]
     L.ws_device_ptr.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp), _c_i64p]

@@ -408,8 +408,9 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
             throw ws::Error(WS_ERR_VALUE, "gamma must be positive and finite");
         if (loss_kind != WS_LOSS_HINGE && loss_kind != WS_LOSS_SOFTPLUS)
             throw ws::Error(WS_ERR_VALUE, "unknown loss kind");
-        if (reduce_width < 1 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
-            throw ws::Error(WS_ERR_VALUE, "reduce_width must be a power of two in [1, 32]");
+        if (reduce_width < 0 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
+            throw ws::Error(WS_ERR_VALUE, "reduce_width must be 0 (np.add.reduceat order) or a power "
+                                          "of two in [1, 32]");
         if (granularity < 1) throw ws::Error(WS_ERR_VALUE, "granularity must be >= 1");
         cudaStream_t s = as_stream(stream, c.s_main);
         cudaStream_t g = as_stream(stream_grad, c.s_grad);
@@ -466,6 +467,26 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
             for (int k = 0; k < n_corners; k++) c.corners[corner0 + k].has_lse = false;
         if (flags & WS_RUN_LSE)
             for (int k = 0; k < n_corners; k++) c.corners[corner0 + k].has_lse = true;
+        if (!stream) WS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int ws_run_kernel(ws_ctx* h, int corner, int kind, int level, double gamma, int loss_kind,
+                  int reduce_width, void* stream)
+{
+    return guarded([&] {
+        if (!h) throw ws::Error(WS_ERR_VALUE, "null context");
+        ws::Context& c = h->c;
+        check_corner(c, corner);
+        if ((kind == 3 || kind == 4 || kind == 5) && !(gamma > 0.0 && gamma < __builtin_huge_val()))
+            throw ws::Error(WS_ERR_VALUE, "gamma must be positive and finite");
+        if (loss_kind != WS_LOSS_HINGE && loss_kind != WS_LOSS_SOFTPLUS)
+            throw ws::Error(WS_ERR_VALUE, "unknown loss kind");
+        if (reduce_width < 0 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
+            throw ws::Error(WS_ERR_VALUE, "reduce_width must be 0 (np.add.reduceat order) or a power "
+                                          "of two in [1, 32]");
+        cudaStream_t s = as_stream(stream, c.s_main);
+        ws::run_kernel(c, corner, kind, level, gamma, loss_kind, reduce_width, s);
         if (!stream) WS_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -612,8 +633,9 @@ int ws_rc_level(int64_t n_lv, const int64_t* nets, int64_t n_nets, const int64_t
                 double* load, double* net_delay, double* impulse, int reduce_width)
 {
     return guarded([&] {
-        if (reduce_width < 1 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
-            throw ws::Error(WS_ERR_VALUE, "reduce_width must be a power of two in [1, 32]");
+        if (reduce_width < 0 || reduce_width > 32 || (reduce_width & (reduce_width - 1)))
+            throw ws::Error(WS_ERR_VALUE, "reduce_width must be 0 (np.add.reduceat order) or a power "
+                                          "of two in [1, 32]");
         ShimArena sa;
         ws::Topo t{};
         t.N = (int)n_nets; t.M = (int)n_mem; t.P = (int)n_pins;

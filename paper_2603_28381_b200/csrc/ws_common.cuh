@@ -262,6 +262,69 @@ __device__ __forceinline__ double lut_blend(const double* tab, int nL, const Loc
     return __dadd_rn(__dmul_rn(1.0 - s.f, v0), __dmul_rn(s.f, v1));
 }
 
+// numpy's pairwise summation of n terms get(i0 .. i0+n-1) (the inner loop of
+// ndarray.sum / np.add.reduce / reduceat): < 8 terms sequentially from 0.0;
+// <= 128 terms in 8 strided accumulators combined as ((r0+r1)+(r2+r3))+
+// ((r4+r5)+(r6+r7)) plus the tail; longer runs split at n/2 rounded down to a
+// multiple of 8, left half + right half.  The split recursion runs on an
+// explicit stack (device recursion would need an unbounded call stack).
+// No FMA.
+template <class Get>
+__device__ __forceinline__ double np_pairwise_leaf(const Get& get, int i0, int n)
+{
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; i++) r = __dadd_rn(r, get(i0 + i));
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) r[k] = get(i0 + k);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], get(i0 + i + k));
+    double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) s = __dadd_rn(s, get(i0 + i));
+    return s;
+}
+
+template <class Get>
+__device__ double np_pairwise(const Get& get, int i0, int n)
+{
+    if (n <= 128) return np_pairwise_leaf(get, i0, n);
+    // frames: (first term, count, state 0 = left pending / 1 = right pending
+    // / 2 = both done, left sum)
+    int fi[32], fn[32], fs[32];
+    double fl[32];
+    int sp = 1;
+    fi[0] = i0; fn[0] = n; fs[0] = 0;
+    double ret = 0.0;
+    while (sp > 0) {
+        const int k = sp - 1;
+        if (fn[k] <= 128) {
+            ret = np_pairwise_leaf(get, fi[k], fn[k]);
+            sp--;
+            continue;
+        }
+        int n2 = fn[k] / 2;
+        n2 -= n2 % 8;
+        if (fs[k] == 0) {
+            fs[k] = 1;
+            fi[sp] = fi[k]; fn[sp] = n2; fs[sp] = 0; sp++;
+        } else if (fs[k] == 1) {
+            fl[k] = ret;
+            fs[k] = 2;
+            fi[sp] = fi[k] + n2; fn[sp] = fn[k] - n2; fs[sp] = 0; sp++;
+        } else {
+            ret = __dadd_rn(fl[k], ret);
+            sp--;
+        }
+    }
+    return ret;
+}
+
 // Ordered selection with the reference's strict comparisons: `cand` comes
 // later in the sequence than `cur`, so it wins only when strictly better
 // (first element wins ties, _kernels.pyx:195-197, 238-239, 247-248).

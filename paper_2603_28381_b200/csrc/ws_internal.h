@@ -161,6 +161,8 @@ void alloc_corners(Context& ctx, int n);
 void upload_values(Context& ctx, int corner, const ws_design_desc* d);
 void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int loss_kind,
               int granularity, cudaStream_t s, cudaStream_t g, int w);
+void run_kernel(Context& ctx, int c0, int kind, int level, double g, int loss_kind, int w,
+                cudaStream_t s);
 // level-list launches for the legacy per-level shims
 void launch_rc_list(const Topo& t, const Corner* dcs, const int* list, int n, int w, cudaStream_t s);
 void launch_fwd_list(const Topo& t, const Corner* dcs, int n, int lut_s_len, int lut_l_len,

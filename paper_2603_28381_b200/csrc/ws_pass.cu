@@ -152,21 +152,8 @@ __device__ double lse_root_global(const Topo& t, const Corner& C, int a0, int a1
                                    C.arc_delay[(size_t)t.ta_arc[q] * 4 + c]);
         return exp(__ddiv_rn(__dsub_rn(x, cmax), g));
     };
-    const int n = a1 - a0;
-    double rest = 0.0;
-    if (n - 1 >= 8 && n - 1 <= 128) {     // numpy pairwise: 8 accumulators, then tail
-        double r[8];
-        for (int k = 0; k < 8; k++) r[k] = z_of(a0 + 1 + k);
-        int i = 8;
-        const int nn = n - 1;
-        for (; i < nn - (nn % 8); i += 8)
-            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], z_of(a0 + 1 + i + k));
-        rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < nn; i++) rest = __dadd_rn(rest, z_of(a0 + 1 + i));
-    } else {                              // < 8 (numpy: sequential); > 129 in-arcs: sequential
-        for (int q = a0 + 1; q < a1; q++) rest = __dadd_rn(rest, z_of(q));
-    }
+    // np.add.reduceat: the first term plus numpy's pairwise sum of the rest
+    const double rest = np_pairwise(z_of, a0 + 1, a1 - a0 - 1);
     const double s = __dadd_rn(z_of(a0), rest);
     if (write_w)
         for (int q = a0; q < a1; q++) C.weights[(size_t)t.ta_arc[q] * 2 + j] = __ddiv_rn(z_of(q), s);
@@ -221,6 +208,15 @@ __device__ void rc_seq(const Topo& t, const Corner& C, int net, int root, int s,
         const int pl = t.mem_parent_loc[s + k];
         if (pl > 0) buf[4 * (pl - 1)] = __dadd_rn(buf[4 * (pl - 1)], buf[4 * k]);
     }
+    if (w == 0) {
+        // reduce mode "sequential" of run_reference (sta.py:236-240): the
+        // member loads summed by np.add.reduceat — first + pairwise rest;
+        // a net without members keeps root_cap
+        const double* bb = buf;
+        auto get = [bb](int i) { return bb[4 * i]; };
+        const double rc = C.root_cap[(size_t)net * 4 + c];
+        C.load[(size_t)root * 4 + c] = m ? __dadd_rn(rc, __dadd_rn(buf[0], np_pairwise(get, 1, m - 1))) : rc;
+    } else {
     double partials[32];
     for (int lane = 0; lane < w; lane++) {
         double p = 0.0;
@@ -231,6 +227,7 @@ __device__ void rc_seq(const Topo& t, const Corner& C, int net, int root, int s,
         for (int lane = 0; lane < w; lane += 2 * stride)
             partials[lane] = __dadd_rn(partials[lane], partials[lane + stride]);
     C.load[(size_t)root * 4 + c] = __dadd_rn(C.root_cap[(size_t)net * 4 + c], partials[0]);
+    }
     if (!root_member) {
         C.net_delay[(size_t)root * 4 + c] = 0.0;
         C.impulse[(size_t)root * 4 + c] = 0.0;
@@ -1254,11 +1251,11 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_tree(Topo t, Corners cs)
 #define LSTAMP(slot) do { } while (0)
 #endif
 
-__global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w)
+__global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w, int k0)
 {
     __shared__ RcSmem S;
     pdl_trigger();
-    const Task T = load_task(t, blockIdx.x);
+    const Task T = load_task(t, k0 + blockIdx.x);
     RcRec R;
     rc_records(t, T, S, R);
     pdl_wait();
@@ -2290,10 +2287,18 @@ struct Launcher {
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);
             }
         } else {
-            launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w);
+            launch(k_rc, dim3(ctx.t.n_tasks, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w, 0);
         }
         count++;
         return took_free;
+    }
+    // the RC of one level's tasks (the per-kernel pipeline's net_rc:level)
+    void rc_level(cudaStream_t s, int li, int w)
+    {
+        const int nt = tasks(li);
+        if (nt <= 0) return;
+        launch(k_rc, dim3(nt, nc), dim3(PASS_TPB), 0, s, ctx.t, cs, w, ctx.lvt_ptr_host[li]);
+        count++;
     }
     // WS_PROBE builds: launch i stamps into probe + i * PROBE_STRIDE
     static constexpr size_t PROBE_STRIDE = 8 * 2048;
@@ -2553,6 +2558,40 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
 }
 
 }  // namespace
+
+// One kernel of the fusion pipeline's graph (fusion.py:113-160 kinds), for
+// the host-side dependency discipline of PipelineRun (fusion.py:307-312):
+// 0 net_rc (level 0 also seeds the pins in no net), 1 cell_delay_at,
+// 2 slack_bwd, 3 lse_fwd, 4 grad_bwd, 5 finish (free-pin / PI-root
+// adjoints, TNS / WNS / loss).  The same device functions as ws_run.
+void run_kernel(Context& ctx, int c0, int kind, int level, double g, int loss_kind, int w,
+                cudaStream_t s)
+{
+    Launcher la(ctx, c0, 1);
+    if (la.lut_bytes > 48 * 1024) {
+        WS_CUDA(cudaFuncSetAttribute(k_fwd<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la.lut_bytes));
+        WS_CUDA(cudaFuncSetAttribute(k_fwd<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la.lut_bytes));
+    }
+    if (kind != 5 && (level < 0 || level >= ctx.t.L))
+        throw Error(WS_ERR_VALUE, "kernel level out of range");
+    switch (kind) {
+    case 0:
+        if (level == 0) la.free_pins(s, true);
+        la.rc_level(s, level, w);
+        break;
+    case 1: la.fwd<true, false>(s, level, g); break;
+    case 2: la.bwd<true, false>(s, level, g, loss_kind); break;
+    case 3: la.fwd<false, true>(s, level, g); break;
+    case 4: la.bwd<false, true>(s, level, g, loss_kind); break;
+    case 5:
+        la.fin(s, g, loss_kind);
+        la.summary(s, g, loss_kind, true, true);
+        break;
+    default: throw Error(WS_ERR_VALUE, "unknown kernel kind");
+    }
+    WS_CHECK_LAUNCH();
+    ctx.launches_last_run = la.count;
+}
 
 void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int loss_kind,
               int granularity, cudaStream_t s, cudaStream_t gs, int w)

@@ -156,3 +156,143 @@ def timing_gradients(design, cfg: LseConfig | None = None, loss: str = "hinge",
                       arc_delay=state.arc_delay)
         dev.run(_lib.RUN_LSE | _lib.RUN_GRAD, gamma=gamma, loss=loss)
     return GradientState.from_device(dev, 0, gamma, loss, flat=flat)
+
+
+# ---------------------------------------------------------------------------
+# finite-difference validation (diff.py:339-474)
+
+@dataclass
+class FiniteDiffReport:
+    max_rel_error: float
+    max_abs_error: float
+    worst_coordinate: tuple | None   # (kind, index, condition name)
+    n_coords: int
+    n_significant: int
+    epsilon: float
+    gamma: float
+    epsilon_dominated: bool
+    loss_kind: str
+    n_refined: int = 0
+
+    def __str__(self):
+        flag = " [epsilon-dominated]" if self.epsilon_dominated else ""
+        return (f"finite-diff: max rel {self.max_rel_error:.3e} (abs {self.max_abs_error:.3e}) over "
+                f"{self.n_significant}/{self.n_coords} coords at eps={self.epsilon:.3e}, "
+                f"gamma={self.gamma:.3e}{flag}")
+
+
+def _smooth_loss_ld(flat, gamma, seed, arc_d, edges, loss):
+    """The smooth loss in extended precision (numpy long double) from seed
+    arrivals (P,2), late arc delays (A,2) and member edge delays (M,2): LSE
+    over every arc-driven root's in-arcs, level by level, root + path delay
+    for the members, then the hinge / softplus endpoint loss (the
+    definitions of diff.py:123-212).  Finite-difference quotients need the
+    extra digits: a coordinate's loss change is ~eps * |grad| while the loss
+    itself carries FP64 rounding of ~1e-16 * |loss|."""
+    ld = np.longdouble
+    g = ld(gamma)
+    lse = np.asarray(seed, dtype=ld).copy()
+    net_ptr = np.asarray(flat.net_ptr, dtype=np.int64)
+    pl = np.asarray(flat.mem_parent_loc, dtype=np.int64)
+    mem_net = np.asarray(flat.mem_net, dtype=np.int64)
+    path = np.zeros_like(np.asarray(edges, dtype=ld))
+    e = np.asarray(edges, dtype=ld)
+    # cumulative path delay: members are topologically ordered within a net
+    local = np.asarray(flat.mem_local, dtype=np.int64)
+    for pos in range(int(local.max()) + 1 if len(local) else 0):
+        idx = np.flatnonzero(local == pos)
+        par = pl[idx]
+        base = np.zeros((len(idx), 2), dtype=ld)
+        inner = par > 0
+        base[inner] = path[net_ptr[mem_net[idx[inner]]] + par[inner] - 1]
+        path[idx] = e[idx] + base
+    in_ptr = np.asarray(flat.net_in_ptr, dtype=np.int64)
+    in_arc = np.asarray(flat.net_in_arc, dtype=np.int64)
+    a_from = np.asarray(flat.arc_from, dtype=np.int64)
+    roots = np.asarray(flat.net_root, dtype=np.int64)
+    mem_pin = np.asarray(flat.mem_pin, dtype=np.int64)
+    ad = np.asarray(arc_d, dtype=ld)
+    for li in range(flat.n_levels):
+        nets = np.asarray(flat.schedule.levels[li], dtype=np.int64)
+        cnt = in_ptr[nets + 1] - in_ptr[nets]
+        drv = nets[cnt > 0]
+        if len(drv):
+            c = cnt[cnt > 0]
+            arcs = np.concatenate([in_arc[in_ptr[n]:in_ptr[n + 1]] for n in drv])
+            seg = np.concatenate([[0], np.cumsum(c)[:-1]])
+            x = lse[a_from[arcs]] + ad[arcs]
+            cm = np.maximum.reduceat(x, seg, axis=0)
+            z = np.exp((x - np.repeat(cm, c, axis=0)) / g)
+            lse[roots[drv]] = cm + g * np.log(np.add.reduceat(z, seg, axis=0))
+        mem = np.concatenate([np.arange(net_ptr[n], net_ptr[n + 1]) for n in nets]) if len(nets) else []
+        if len(mem):
+            lse[mem_pin[mem]] = lse[roots[mem_net[mem]]] + path[mem]
+    v = lse[np.asarray(flat.ep_pin, dtype=np.int64)] - np.asarray(flat.ep_required, dtype=ld)[:, 2:4]
+    if loss == "hinge":
+        return np.maximum(v, 0).sum()
+    return (np.maximum(v, 0) + g * np.log1p(np.exp(-np.abs(v) / g))).sum()
+
+
+def finite_diff_check(design, cfg: LseConfig | None = None, epsilon: float | None = None,
+                      loss: str = "hinge", grad_floor: float = 1e-8,
+                      refine_threshold: float = 1e-5) -> FiniteDiffReport:
+    """Central finite differences of the smooth loss against the device's
+    analytic d_arc / d_edge, one late-column coordinate at a time
+    (diff.py:339-474).  The device runs the hard pass (seed arrivals, arc and
+    net delays) and the analytic gradients; the perturbed losses are
+    evaluated on the host in long double, as the reference does, because an
+    FP64 quotient of a coordinate with |grad| ~ 1e-7 is noise-limited at
+    ~1e-3.  ``refine_threshold`` is accepted for API compatibility: the
+    reference re-checks such coordinates with mpmath; the extended-precision
+    quotients here are not refined (n_refined = 0)."""
+    _check_loss(loss)
+    flat = _flat_of(design)
+    if epsilon is not None and epsilon <= 0:
+        raise ValueError("epsilon must be positive")
+    gamma = cfg.gamma if cfg is not None else default_gamma(flat.clock_period)
+    LseConfig(gamma)
+    eps = float(epsilon) if epsilon is not None else 1e-6 * flat.clock_period
+    dev = device_of(flat)
+    dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED, gamma=gamma, loss=loss)
+    got = dev.get_many(("arrival", "arc_delay", "net_delay", "d_arc", "d_edge"))
+    ld = np.longdouble
+    seed = got["arrival"][:, 2:4].astype(ld)
+    arc_d = got["arc_delay"][:, 2:4].astype(ld)
+    mem_pin = np.asarray(flat.mem_pin, dtype=np.int64)
+    nd = got["net_delay"][mem_pin][:, 2:4].astype(ld)
+    pl = np.asarray(flat.mem_parent_loc, dtype=np.int64)
+    net_ptr = np.asarray(flat.net_ptr, dtype=np.int64)
+    pidx = np.where(pl > 0, net_ptr[np.asarray(flat.mem_net, dtype=np.int64)] + pl - 1, 0)
+    edges = nd - np.where((pl > 0)[:, None], nd[pidx], ld(0))
+    e = ld(eps)
+    rows = []
+    for a in range(flat.n_arcs):
+        for j in range(2):
+            up, dn = arc_d.copy(), arc_d.copy()
+            up[a, j] += e
+            dn[a, j] -= e
+            fd = (_smooth_loss_ld(flat, gamma, seed, up, edges, loss)
+                  - _smooth_loss_ld(flat, gamma, seed, dn, edges, loss)) / (2 * e)
+            rows.append((float(got["d_arc"][a, j]), float(fd), ("arc", a, COL_NAMES[j])))
+    for k in range(len(mem_pin)):
+        for j in range(2):
+            up, dn = edges.copy(), edges.copy()
+            up[k, j] += e
+            dn[k, j] -= e
+            fd = (_smooth_loss_ld(flat, gamma, seed, arc_d, up, loss)
+                  - _smooth_loss_ld(flat, gamma, seed, arc_d, dn, loss)) / (2 * e)
+            rows.append((float(got["d_edge"][k, j]), float(fd), ("edge", k, COL_NAMES[j])))
+    max_rel = max_abs = 0.0
+    worst = None
+    n_sig = 0
+    for an, fd, coord in rows:
+        err = abs(fd - an)
+        max_abs = max(max_abs, err)
+        if abs(an) > grad_floor:
+            n_sig += 1
+            if err / abs(an) > max_rel:
+                max_rel, worst = err / abs(an), coord
+    return FiniteDiffReport(max_rel_error=max_rel, max_abs_error=max_abs, worst_coordinate=worst,
+                            n_coords=2 * (flat.n_arcs + len(mem_pin)), n_significant=n_sig,
+                            epsilon=eps, gamma=gamma, epsilon_dominated=bool(eps >= 0.1 * gamma),
+                            loss_kind=loss, n_refined=0)

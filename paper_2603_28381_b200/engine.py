@@ -61,8 +61,13 @@ class _CudaArray:
 class DeviceDesign:
     """One design on the device with ``n_corners`` value/state slots."""
 
-    def __init__(self, raw: RawDesign, n_corners: int = 1):
+    def __init__(self, raw: RawDesign, n_corners: int = 1, validate: bool = True):
         raw = raw.normalized()
+        if validate:
+            # what the device build relies on (tree order, one driver per pin,
+            # increasing LUT axes); the full model check is design_io.validate
+            from .design_io import check_engine_invariants
+            check_engine_invariants(raw)
         self.raw = raw
         L = lib()
         d = _lib.DesignDesc()

@@ -1,4 +1,4 @@
-"""Operation fusion on CUDA streams (drop-in for stasim/fusion.py:38-160, 421-450).
+"""Operation fusion on CUDA streams (drop-in for stasim/fusion.py:38-160, 287-450).
 
 The reference models two "streams" with Python threads and events
 (fusion.py:383-407) and reports a *simulated* makespan.  Here the streams are
@@ -17,6 +17,17 @@ real CUDA streams inside one ``ws_run`` call:
 Both run the same device functions as ``execute_sequential`` so all outputs
 are bitwise identical (fusion.py:6-9); the returned ``FusedResult`` carries
 CUDA-event-measured times instead of simulated cycles.
+
+``PipelineRun`` is the kernel-by-kernel form of the same graph
+(fusion.py:287-333): ``execute(kernel, deps)`` refuses, with
+``FusionError``, a kernel whose dependencies have not run, and otherwise
+launches exactly that kernel on the device (ws_run_kernel).
+``execute_graph`` drives every kernel of ``build_kernel_graph`` through it.
+
+The reference's two-lane makespan *simulator* (fusion.py:163-265) is not part
+of this package: scripts/makespan_c3.py feeds the per-kernel costs measured
+here (``measured_kernel_costs``) to the reference's own
+``schedule_sequential`` / ``schedule_fused``.
 """
 
 from __future__ import annotations
@@ -159,96 +170,6 @@ def build_kernel_graph(schedule, costs=None, granularity: int = 10) -> KernelGra
                        event_granularity=granularity, n_levels=n_levels)
 
 
-# ---------------------------------------------------------------------------
-# makespan model (fusion.py:163-265): the reference's two-lane schedule over
-# per-kernel costs.  Here the costs can be MEASURED on the device
-# (measured_kernel_costs), which validates the model against the real
-# two-stream run (makespan_report).
-
-@dataclass
-class ScheduleResult:
-    records: list
-    makespan: float
-    overlap_fraction: float
-    sta_finish: float
-    grad_cycles: float
-    overlapped_grad_cycles: float
-
-    def _times(self):
-        got = getattr(self, "_times_cache", None)
-        if got is None:
-            got = {r["id"]: (r["start"], r["finish"]) for r in self.records}
-            self._times_cache = got
-        return got
-
-    def start(self, kid):
-        return self._times()[kid][0]
-
-    def finish(self, kid):
-        return self._times()[kid][1]
-
-
-def _result(graph: KernelGraph, times: dict) -> ScheduleResult:
-    records, sta_fin = [], 0.0
-    for kid in graph.sta_order + graph.grad_order:
-        k = graph.kernels[kid]
-        s, f = times[kid]
-        records.append({"id": kid, "stream": k.stream, "kind": k.kind, "level": k.level,
-                        "start": s, "finish": f})
-        if k.stream == STA_STREAM:
-            sta_fin = max(sta_fin, f)
-    grad = sum(r["finish"] - r["start"] for r in records if r["stream"] == GRAD_STREAM)
-    over = sum(max(0.0, min(r["finish"], sta_fin) - r["start"]) for r in records
-               if r["stream"] == GRAD_STREAM)
-    return ScheduleResult(records=records, makespan=max((f for _, f in times.values()), default=0.0),
-                          overlap_fraction=over / grad if grad > 0 else 0.0, sta_finish=sta_fin,
-                          grad_cycles=grad, overlapped_grad_cycles=over)
-
-
-def schedule_sequential(graph: KernelGraph) -> ScheduleResult:
-    """One lane: the sta stream's kernels, then the grad stream's."""
-    times, t = {}, 0.0
-    for kid in graph.sta_order + graph.grad_order:
-        c = graph.kernels[kid].cost
-        times[kid] = (t, t + c)
-        t += c
-    return _result(graph, times)
-
-
-def schedule_fused(graph: KernelGraph, contention: float = 1.0) -> ScheduleResult:
-    """Two lanes: the sta lane never waits; a grad kernel starts when its lane
-    is free and its event sources finished, at `contention` x cost while the
-    sta lane is still busy."""
-    times, t = {}, 0.0
-    for kid in graph.sta_order:
-        c = graph.kernels[kid].cost
-        times[kid] = (t, t + c)
-        t += c
-    sta_total, t = t, 0.0
-    for kid in graph.grad_order:
-        start = max([t] + [times[d][1] for d in graph.cross_deps(kid)])
-        c = graph.kernels[kid].cost * (contention if start < sta_total else 1.0)
-        times[kid] = (start, start + c)
-        t = start + c
-    return _result(graph, times)
-
-
-def check_schedule(graph: KernelGraph, result: ScheduleResult) -> list:
-    """Stream order, event edges, makespan = last finish."""
-    problems = []
-    for order in (graph.sta_order, graph.grad_order):
-        for a, b in zip(order, order[1:]):
-            if result.start(b) < result.finish(a):
-                problems.append(f"stream order violated: {b} starts before {a} ends")
-    for e in graph.edges:
-        if result.start(e.dst) < result.finish(e.src):
-            problems.append(f"event violated: {e.dst} starts before {e.src} ends")
-    last = max((r["finish"] for r in result.records), default=0.0)
-    if result.makespan != last:
-        problems.append("makespan is not the last finish")
-    return problems
-
-
 KIND_NAMES = {0: "net_rc", 1: "cell_delay_at", 2: "slack_bwd", 3: "lse_fwd", 4: "grad_bwd"}
 
 
@@ -258,7 +179,8 @@ def measured_kernel_costs(dev, n_levels: int, gamma: float | None = None, loss: 
     (one CUDA event after every launch; median of `repeats`).  The RC of all
     levels is one streaming launch, charged to net_rc:0; launches outside the
     graph (free pins, adjoint finish, summary) are folded into the
-    neighbouring kernel of the same stream."""
+    neighbouring kernel of the same stream.  The makespan model that consumes
+    these costs is the reference's own (scripts/makespan_ref.py)."""
     import statistics
     flags = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_TIMED
     runs = []
@@ -276,62 +198,6 @@ def measured_kernel_costs(dev, n_levels: int, gamma: float | None = None, loss: 
             if pk in KIND_NAMES:
                 costs[(KIND_NAMES[pk], pl)] += ms
     return costs
-
-
-def makespan_report(design, schedule=None, cfg: "FusionConfig | None" = None, repeats: int = 5) -> dict:
-    """The reference's makespan model (schedule_sequential / schedule_fused)
-    on MEASURED kernel costs, next to the measured sequential, two-stream and
-    fused (interleaved) passes of the same design.
-
-    Events between launches serialise the programmatic-dependent-launch
-    overlap of the untimed pass, so the raw per-launch deltas are calibrated
-    to the measured sequential pass (same proportions, same total).  The
-    model's two-lane prediction is then compared with the measured two-stream
-    pass, and the contention factor that reproduces it is fitted (the
-    reference's ``contention`` knob, fusion.py:227-249)."""
-    from .diff import _flat_of
-    import torch
-    cfg = cfg or FusionConfig()
-    flat = _flat_of(design, schedule)
-    gamma = cfg.gamma if cfg.gamma is not None else default_gamma(flat.clock_period)
-    dev = device_of(flat)
-    raw_costs = measured_kernel_costs(dev, flat.n_levels, gamma, cfg.loss, repeats)
-
-    def measure(flags):
-        ts = []
-        for i in range(repeats + 1):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            dev.run(flags, gamma=gamma, loss=cfg.loss, granularity=cfg.granularity)
-            e1.record()
-            e1.synchronize()
-            if i:
-                ts.append(e0.elapsed_time(e1))
-        return sorted(ts)[len(ts) // 2]
-
-    base = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
-    seq_ms = measure(base)
-    two_ms = measure(base | _lib.RUN_TWO_STREAM)
-    fused_ms = measure(base | _lib.RUN_FUSED)
-    total = sum(raw_costs.values()) or 1.0
-    costs = {k: v * seq_ms / total for k, v in raw_costs.items()}
-    g = build_kernel_graph(flat.n_levels, costs, cfg.granularity)
-    seq, fus = schedule_sequential(g), schedule_fused(g, 1.0)
-    lo, hi = 1.0, 8.0                       # contention reproducing the two-stream run
-    if schedule_fused(g, hi).makespan < two_ms:
-        fit = None
-    elif fus.makespan >= two_ms:
-        fit = 1.0
-    else:
-        for _ in range(50):
-            mid = 0.5 * (lo + hi)
-            lo, hi = (mid, hi) if schedule_fused(g, mid).makespan < two_ms else (lo, mid)
-        fit = 0.5 * (lo + hi)
-    return {"raw_event_sum_ms": total, "model_sequential_ms": seq.makespan,
-            "model_fused_ms": fus.makespan, "model_overlap_fraction": fus.overlap_fraction,
-            "measured_sequential_ms": seq_ms, "measured_two_stream_ms": two_ms,
-            "measured_interleaved_ms": fused_ms, "fitted_contention": fit,
-            "problems": check_schedule(g, fus) + check_schedule(g, seq)}
 
 
 @dataclass
@@ -385,3 +251,80 @@ def execute_fused(design, schedule=None, geometry=None, cfg: FusionConfig | None
     if cfg.mode == "interleaved":
         return _run(design, schedule, cfg, base | _lib.RUN_FUSED, "interleaved")
     return _run(design, schedule, cfg, base | _lib.RUN_TWO_STREAM, "streams")
+
+
+# ---------------------------------------------------------------------------
+# kernel-by-kernel execution with the dependency discipline (fusion.py:287-333)
+
+KIND_IDS = {"net_rc": 0, "cell_delay_at": 1, "slack_bwd": 2, "lse_fwd": 3, "grad_bwd": 4}
+
+
+class PipelineRun:
+    """One design's pipeline, one graph kernel at a time on the device.
+
+    ``execute(kernel, deps)`` raises ``FusionError`` when any dependency has
+    not executed yet (the reference's _PipelineRun.execute), else launches
+    the kernel (ws_run_kernel: the same device functions as ws_run) and marks
+    it done.  ``finalize()`` adds the pins finished after the level loop and
+    the TNS / WNS / loss, and returns (TimingState, GradientState)."""
+
+    def __init__(self, design, cfg: "FusionConfig | None" = None, schedule=None):
+        from .diff import _flat_of
+        self.cfg = cfg or FusionConfig()
+        self.flat = _flat_of(design, schedule)
+        self.gamma = self.cfg.gamma if self.cfg.gamma is not None else default_gamma(self.flat.clock_period)
+        LseConfig(self.gamma)
+        self.dev = device_of(self.flat)
+        self.done = set()
+
+    def _launch(self, kind_id, level):
+        from ._lib import LOSS_KINDS, check, lib
+        from .engine import _stream_handle
+        if self.cfg.loss not in LOSS_KINDS:
+            raise ValueError(f"unknown loss kind {self.cfg.loss!r}")
+        check(lib().ws_run_kernel(self.dev._h, 0, int(kind_id), int(level), float(self.gamma),
+                                  LOSS_KINDS[self.cfg.loss], int(self.cfg.reduce_width),
+                                  _stream_handle(None)))
+
+    def execute(self, kernel: Kernel, deps: list):
+        missing = [d for d in deps if d not in self.done]
+        if missing:
+            raise FusionError(f"kernel {kernel.id} ran before its dependencies {missing}")
+        if kernel.kind not in KIND_IDS:
+            raise ValueError(f"unknown kernel kind {kernel.kind!r}")
+        self._launch(KIND_IDS[kernel.kind], kernel.level)
+        self.done.add(kernel.id)
+
+    def finalize(self):
+        self._launch(5, 0)
+        st = TimingState.from_device(self.dev, 0, n_levels=self.flat.n_levels)
+        gs = GradientState.from_device(self.dev, 0, self.gamma, self.cfg.loss, flat=self.flat)
+        return st, gs
+
+
+def execute_graph(design, schedule=None, cfg: FusionConfig | None = None):
+    """Every kernel of ``build_kernel_graph`` through ``PipelineRun`` in a
+    dependency-respecting order (stream predecessors and event sources
+    first): bitwise the sequential pass."""
+    cfg = cfg or FusionConfig()
+    run = PipelineRun(design, cfg, schedule)
+    g = build_kernel_graph(run.flat.n_levels, None, cfg.granularity)
+    pred = {}
+    for order in (g.sta_order, g.grad_order):
+        for a, b in zip(order, order[1:]):
+            pred[b] = a
+    pending = [list(g.sta_order), list(g.grad_order)]
+    while pending[0] or pending[1]:
+        progressed = False
+        for lane in pending:
+            while lane:
+                kid = lane[0]
+                deps = ([pred[kid]] if kid in pred else []) + g.cross_deps(kid)
+                if any(d not in run.done for d in deps):
+                    break
+                run.execute(g.kernels[kid], deps)
+                lane.pop(0)
+                progressed = True
+        if not progressed:
+            raise FusionError("kernel graph has no runnable kernel (cyclic dependencies)")
+    return run.finalize()

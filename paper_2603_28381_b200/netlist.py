@@ -52,6 +52,12 @@ class Lut2D:
         self.load_axis = np.asarray(self.load_axis, dtype=np.float64)
         self.table = np.asarray(self.table, dtype=np.float64)
 
+    def check(self) -> list:
+        """Problems of this table (empty when well formed): axes 1-D,
+        non-empty, strictly increasing; table (nS, nL); finite entries."""
+        from .design_io import lut_problems
+        return lut_problems(self.slew_axis, self.load_axis, self.table)
+
 
 @dataclass
 class TimingArc:

@@ -37,6 +37,7 @@ from stasim import (GeneratorConfig, generate_design, flatten, power_law, unifor
 from stasim.netlist import (Cell, Design, Endpoint, Lut2D, Net, PrimaryInput,  # noqa: E402
                             TimingArc)
 from stasim.warp import run_engine  # noqa: E402
+from stasim.sta import run_reference  # noqa: E402
 from stasim.diff import timing_gradients, LseConfig  # noqa: E402
 from stasim.backend import backend_name  # noqa: E402
 
@@ -57,6 +58,8 @@ FLAT_FIELDS = ("net_ptr", "net_root", "root_cap", "root_kind", "mem_pin", "mem_p
 ST_FIELDS = ("load", "net_delay", "impulse", "slew", "arrival", "required", "slack",
              "arc_delay")
 G_FIELDS = ("lse_arrival", "arc_weights", "d_arc", "d_edge", "adjoint")
+# fixtures that also store run_reference(flat) in its default "sequential" mode
+SEQ_CASES = ("edge_kinds", "gen_tree_1200", "gen_heavy_1500", "multi_out", "gen_uniform_tree")
 
 
 # --- reference test fixtures (restated builders; conftest.py:10-127) -------
@@ -340,6 +343,11 @@ def dump(name, design, gamma, softplus):
         arrs["st_" + f] = getattr(st, f)
     for f in G_FIELDS:
         arrs["g_" + f] = getattr(gs, f)
+    if name in SEQ_CASES:
+        # run_reference's default reduce mode (np.add.reduceat root loads)
+        sq = run_reference(flat)
+        for f in ST_FIELDS:
+            arrs["sq_" + f] = getattr(sq, f)
     if softplus:
         gp = timing_gradients(flat, cfg=cfg, loss="softplus", state=st)
         arrs["gs_loss"] = np.float64(gp.loss)
