@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <string>
+#include <unordered_map>
 
 #include "ws_internal.h"
 
@@ -215,7 +217,7 @@ __global__ void k_tq(int N, const int* lv_nets, const int* net_root, const int* 
 __global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* tq_root,
                      const int* net_in_ptr, const int* net_in_arc, const int* arc_from,
                      const int* arc_dlut, const int* arc_slut, int* ta_arc, int* ta_from,
-                     int* ta_root, ushort4* ta_lut)
+                     int* ta_root, int4* ta_lut)
 {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N) return;
@@ -228,8 +230,8 @@ __global__ void k_ta(int N, const int* lv_nets, const int* tq_aptr, const int* t
         ta_root[t] = tq_root[q];
         const int* d = arc_dlut + 4 * (size_t)a;
         const int* sl = arc_slut + 4 * (size_t)a;
-        ta_lut[2 * (size_t)t] = make_ushort4(d[0], d[1], d[2], d[3]);
-        ta_lut[2 * (size_t)t + 1] = make_ushort4(sl[0], sl[1], sl[2], sl[3]);
+        ta_lut[2 * (size_t)t] = make_int4(d[0], d[1], d[2], d[3]);
+        ta_lut[2 * (size_t)t + 1] = make_int4(sl[0], sl[1], sl[2], sl[3]);
     }
 }
 
@@ -384,12 +386,12 @@ int reduce_max(Scratch& sc, Arena& ar, const int* a, int n, cudaStream_t s)
 }
 
 // delay LUT ids of each task net's first in-arc (the root-load locate axis)
-__global__ void k_tq_lut1(int N, const int* tq_aptr, const ushort4* ta_lut, ushort4* out)
+__global__ void k_tq_lut1(int N, const int* tq_aptr, const int4* ta_lut, int4* out)
 {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N) return;
     out[q] = tq_aptr[q + 1] > tq_aptr[q] ? ta_lut[2 * (size_t)tq_aptr[q]]
-                                         : make_ushort4(0xffff, 0xffff, 0xffff, 0xffff);
+                                         : make_int4(-1, -1, -1, -1);
 }
 
 // streaming-RC member code: -1 for members of tree nets (handled per net),
@@ -447,17 +449,17 @@ __global__ void k_blob(Topo t)
         t.bb_q[(size_t)k * TASK_Q + qi] = bq;
         for (int s = 0; s < 3; s++) {
             int2 fa = make_int2(0, 0);
-            uint4 fl = make_uint4(0, 0, 0, 0);
+            int4 fd = make_int4(0, 0, 0, 0), fs = make_int4(0, 0, 0, 0);
             if (fq.w > 0 && fq.w <= 3) {
                 // slots past the last arc repeat arc 0 (branch-free net phase)
                 const int qa = fq.z + (s < fq.w ? s : 0);
                 fa = make_int2(t.ta_from[qa], t.ta_arc[qa]);
-                const ushort4 d = t.ta_lut[2 * (size_t)qa], l = t.ta_lut[2 * (size_t)qa + 1];
-                fl = make_uint4(d.x | ((unsigned)d.y << 16), d.z | ((unsigned)d.w << 16),
-                                l.x | ((unsigned)l.y << 16), l.z | ((unsigned)l.w << 16));
+                fd = t.ta_lut[2 * (size_t)qa];
+                fs = t.ta_lut[2 * (size_t)qa + 1];
             }
             t.fb_a[((size_t)k * TASK_Q + qi) * 3 + s] = fa;
-            t.fb_l[((size_t)k * TASK_Q + qi) * 3 + s] = fl;
+            t.fb_l[2 * (((size_t)k * TASK_Q + qi) * 3 + s)] = fd;
+            t.fb_l[2 * (((size_t)k * TASK_Q + qi) * 3 + s) + 1] = fs;
         }
     }
     if (tid < TASK_M) {
@@ -486,7 +488,6 @@ void build_tasks(Context& ctx)
     Scratch& sc = ctx.scratch;
     cudaStream_t s = ctx.s_main;
     const int N = t.N, M = t.M, P = t.P;
-    if (t.NL > 65535) throw Error(WS_ERR_VALUE, "more than 65535 LUTs in the pool");
     t.tq_root = ar.alloc<int>(N);
     t.tq_flags = ar.alloc<int>(N);
     t.tq_f0 = ar.alloc<int>(N);
@@ -519,7 +520,7 @@ void build_tasks(Context& ctx)
     t.ta_from = ar.alloc<int>(na);
     t.ta_root = ar.alloc<int>(na);
     t.ta_q = ar.alloc<int>(na);
-    t.ta_lut = ar.alloc<ushort4>(2 * (size_t)na);
+    t.ta_lut = ar.alloc<int4>(2 * (size_t)na);
     t.tm_pin = ar.alloc<int>(M);
     t.tm_flags = ar.alloc<int>(M);
     t.tm_optr = ar.alloc<int>(M + 1);
@@ -538,7 +539,7 @@ void build_tasks(Context& ctx)
                                            t.tm_flags, t.tm_o1_to, t.tm_o1_arc, t.tm_e1, ocnt);
         WS_CHECK_LAUNCH();
     }
-    t.tq_lut1 = ar.alloc<ushort4>(N);
+    t.tq_lut1 = ar.alloc<int4>(N);
     if (N) {
         k_tq_lut1<<<blocks_for(N), TPB, 0, s>>>(N, t.tq_aptr, t.ta_lut, t.tq_lut1);
         WS_CHECK_LAUNCH();
@@ -637,7 +638,7 @@ void build_tasks(Context& ctx)
         t.fb_n = ar.alloc<int4>(T * (TASK_Q + 1) * 2);
         t.fb_q = ar.alloc<int4>(T * TASK_Q);
         t.fb_a = ar.alloc<int2>(T * TASK_Q * 3);
-        t.fb_l = ar.alloc<uint4>(T * TASK_Q * 3);
+        t.fb_l = ar.alloc<int4>(T * TASK_Q * 3 * 2);
         t.fb_m = ar.alloc<int2>(T * TASK_M);
         t.bb_m = ar.alloc<int4>(T * TASK_M * 2);
         t.bb_q = ar.alloc<int4>(T * TASK_Q);
@@ -730,17 +731,16 @@ void build_topology(Context& ctx, const ws_design_desc* d)
         // share one offset, so the level kernels locate a query once for both
         // an arc's delay and slew tables (same result, bit for bit)
         std::vector<int4> info((size_t)std::max<int64_t>(d->n_luts, 1));
+        // (hashed on the axis bytes: O(n) for pools of any size; identical
+        // bits are a stricter test than ==, so merging stays exact)
         auto canon = [](const double* flat, const int32_t* ptr, int64_t nl, std::vector<int>& out) {
             out.assign((size_t)nl, 0);
+            std::unordered_map<std::string, int> first;
+            first.reserve((size_t)nl);
             for (int64_t i = 0; i < nl; i++) {
-                out[(size_t)i] = ptr[i];
-                const int n = ptr[i + 1] - ptr[i];
-                for (int64_t k = 0; k < i; k++)
-                    if (ptr[k + 1] - ptr[k] == n &&
-                        std::equal(flat + ptr[k], flat + ptr[k] + n, flat + ptr[i])) {
-                        out[(size_t)i] = out[(size_t)k];
-                        break;
-                    }
+                const char* b = reinterpret_cast<const char*>(flat + ptr[i]);
+                std::string key(b, sizeof(double) * (size_t)(ptr[i + 1] - ptr[i]));
+                out[(size_t)i] = first.emplace(std::move(key), ptr[i]).first->second;
             }
         };
         std::vector<int> cs_, cl_;

@@ -431,34 +431,66 @@ int ws_run(ws_ctx* h, int corner0, int n_corners, uint32_t flags, double gamma, 
             ensure_dsum(c);
         }
         if (flags & WS_RUN_GRAPH) {
+            // graph cache: one executable per (flags, corners, loss, granularity,
+            // reduce width), least recently used first out beyond
+            // kGraphCache entries.  A new gamma keeps the executable: the
+            // pass is re-captured and its kernel parameters swapped in by
+            // cudaGraphExecUpdate (same topology), no re-instantiation.
             const unsigned key = flags & ~WS_RUN_GRAPH;
-            cudaGraphExec_t exec = nullptr;
-            for (auto& e : c.graphs)
-                if (e.key == key && e.c0 == corner0 && e.nc == n_corners && e.gamma == gamma &&
-                    e.loss == loss_kind && e.gran == granularity * 64 + reduce_width) exec = e.exec;
-            if (!exec) {
-                cudaStream_t cap;
+            const int gran = granularity * 64 + reduce_width;
+            auto capture = [&]() {
+                cudaStream_t cap, capg;
                 WS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-                cudaStream_t capg;
                 WS_CUDA(cudaStreamCreateWithFlags(&capg, cudaStreamNonBlocking));
                 WS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
                 ws::run_pass(c, corner0, n_corners, key, gamma, loss_kind, granularity, cap, capg,
                              reduce_width);
                 cudaGraph_t graph;
                 WS_CUDA(cudaStreamEndCapture(cap, &graph));
-                WS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-                WS_CUDA(cudaGraphDestroy(graph));
                 cudaStreamDestroy(cap);
                 cudaStreamDestroy(capg);
-                c.graphs.push_back({key, corner0, n_corners, gamma, loss_kind,
-                                    granularity * 64 + reduce_width, exec});
-                c.graph_launches.push_back(c.launches_last_run);
+                return graph;
+            };
+            size_t hit = c.graphs.size();
+            for (size_t i = 0; i < c.graphs.size(); i++) {
+                const auto& e = c.graphs[i];
+                if (e.key == key && e.c0 == corner0 && e.nc == n_corners && e.loss == loss_kind &&
+                    e.gran == gran) hit = i;
             }
-            int cnt = 0;
-            for (size_t i = 0; i < c.graphs.size(); i++)
-                if (c.graphs[i].exec == exec) cnt = c.graph_launches[i];
-            WS_CUDA(cudaGraphLaunch(exec, s));
-            c.launches_last_run = cnt;
+            if (hit < c.graphs.size() && c.graphs[hit].gamma != gamma) {
+                cudaGraph_t graph = capture();
+                cudaGraphExecUpdateResultInfo info;
+                const cudaError_t ue = cudaGraphExecUpdate(c.graphs[hit].exec, graph, &info);
+                if (ue != cudaSuccess) {       // topology changed: a fresh executable
+                    cudaGetLastError();
+                    cudaGraphExec_t exec;
+                    WS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+                    cudaGraphExecDestroy(c.graphs[hit].exec);
+                    c.graphs[hit].exec = exec;
+                }
+                WS_CUDA(cudaGraphDestroy(graph));
+                c.graphs[hit].gamma = gamma;
+                c.graph_launches[hit] = c.launches_last_run;
+            } else if (hit == c.graphs.size()) {
+                cudaGraph_t graph = capture();
+                cudaGraphExec_t exec;
+                WS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+                WS_CUDA(cudaGraphDestroy(graph));
+                if (c.graphs.size() >= ws::kGraphCache) {   // evict the least recently used
+                    cudaGraphExecDestroy(c.graphs.front().exec);
+                    c.graphs.erase(c.graphs.begin());
+                    c.graph_launches.erase(c.graph_launches.begin());
+                }
+                c.graphs.push_back({key, corner0, n_corners, gamma, loss_kind, gran, exec});
+                c.graph_launches.push_back(c.launches_last_run);
+                hit = c.graphs.size() - 1;
+            }
+            // most recently used last
+            std::rotate(c.graphs.begin() + hit, c.graphs.begin() + hit + 1, c.graphs.end());
+            std::rotate(c.graph_launches.begin() + hit, c.graph_launches.begin() + hit + 1,
+                        c.graph_launches.end());
+            WS_CUDA(cudaGraphLaunch(c.graphs.back().exec, s));
+            c.launches_last_run = c.graph_launches.back();
         } else {
             ws::run_pass(c, corner0, n_corners, flags, gamma, loss_kind, granularity, s, g,
                          reduce_width);

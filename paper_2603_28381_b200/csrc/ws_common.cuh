@@ -71,8 +71,8 @@ struct Topo {
     int *ta_from;      // [A'] arc source pin
     int *ta_root;      // [A'] root pin of the arc's net
     int *ta_q;         // [A'] index of the arc's net within its task
-    ushort4 *ta_lut;   // [2*A'] delay LUT ids (ER EF LR LF), then slew LUT ids
-    ushort4 *tq_lut1;  // [N] delay LUT ids of q's first in-arc (0xffff: no in-arc)
+    int4 *ta_lut;      // [2*A'] delay LUT ids (ER EF LR LF), then slew LUT ids (32-bit: any pool size)
+    int4 *tq_lut1;     // [N] delay LUT ids of q's first in-arc (-1: no in-arc)
     int *tm_pin;       // [M] member pin
     int *tm_flags;     // [M] TM_* bits | (net index within its task) << 8
     int *tm_optr;      // [M+1] out-arcs of member slot u: to_*[tm_optr[u] .. )
@@ -97,7 +97,7 @@ struct Topo {
     int4 *fb_n;        // [T * (TASK_Q+1) * 2] NetSmem: {root, flags, f0, net}, {e1, aptr, mptr, 0}
     int4 *fb_q;        // [T * TASK_Q] forward net item: {root | -1, flags, a0, na (0: not net-centric)}
     int2 *fb_a;        // [T * TASK_Q * 3] forward in-arc slots: {from, arc}
-    uint4 *fb_l;       // [T * TASK_Q * 3] their delay / slew LUT ids, 2 x 16 bit per word
+    int4 *fb_l;        // [T * TASK_Q * 3 * 2] their delay LUT ids, then slew LUT ids (per cond)
     int2 *fb_m;        // [T * TASK_M] member slots: {pin | -1, tm_flags}
     int4 *bb_m;        // [T * TASK_M * 2] backward member: {pin | -1, fl, o1_to, o1_arc}, {e1, o0, no, arc}
     int4 *bb_q;        // [T * TASK_Q] backward net item: {root | -1, flags, e1, 0}

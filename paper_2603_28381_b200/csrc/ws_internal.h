@@ -117,6 +117,8 @@ struct CornerSlot {
     bool has_lse = false;      // LSE forward done since the last hard pass
 };
 
+constexpr size_t kGraphCache = 16;   // CUDA-graph executables kept per context
+
 struct Context {
     Topo t{};
     CornerStrides cstride{};          // corner k's field = corner 0's + k * stride

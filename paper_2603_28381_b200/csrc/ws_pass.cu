@@ -98,7 +98,7 @@ __device__ double seed_multi(const Topo& t, const Corner& C, int pin, int j, dou
     return a;
 }
 
-__device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
+__device__ __forceinline__ int lut_c(int4 v, int c)
 {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
@@ -413,7 +413,7 @@ struct FwdSmem {
 struct FwdRec {
     int na, a0;                       // the net item's in-arcs: ta_*[a0 .. a0 + na)
     int from[FWD_NA], arc[FWD_NA];
-    unsigned short dl[FWD_NA], sl[FWD_NA];
+    int dl[FWD_NA], sl[FWD_NA];
     int mpin[ITEMS], mfl[ITEMS];
     int nroot, nflags;                // this lane's (net, cond) item
     // pass-static gathers (RC outputs), prefetched by the persistent kernel
@@ -1685,7 +1685,7 @@ struct FwdBlob {
     int4 n[2 * (TASK_Q + 1)];
     int4 q[TASK_Q];
     int2 a[TASK_Q * 3];
-    uint4 l[TASK_Q * 3];
+    int4 l[TASK_Q * 3 * 2];     // delay ids, slew ids (per cond) of each slot
     int2 m[TASK_M];
 };
 struct BwdBlob {
@@ -1736,7 +1736,7 @@ __device__ __forceinline__ void issue_blob(const Topo& t, int k, bool bwd, BlobB
         bulk_g2s(B.f.n, t.fb_n + kn, sizeof(B.f.n), mb);
         bulk_g2s(B.f.q, t.fb_q + (size_t)k * TASK_Q, sizeof(B.f.q), mb);
         bulk_g2s(B.f.a, t.fb_a + (size_t)k * TASK_Q * 3, sizeof(B.f.a), mb);
-        bulk_g2s(B.f.l, t.fb_l + (size_t)k * TASK_Q * 3, sizeof(B.f.l), mb);
+        bulk_g2s(B.f.l, t.fb_l + (size_t)k * TASK_Q * 3 * 2, sizeof(B.f.l), mb);
         bulk_g2s(B.f.m, t.fb_m + (size_t)k * TASK_M, sizeof(B.f.m), mb);
     } else {
         mbar_expect_tx(mb, (unsigned)sizeof(BwdBlob));
@@ -1781,10 +1781,8 @@ __device__ __forceinline__ void fwd_records_smem(const FwdBlob& B, const Task& T
         R.from[s] = fa.x;
         R.arc[s] = fa.y;
         if (HARD) {
-            const uint4 fl = B.l[qi * 3 + s];
-            const unsigned dw = c < 2 ? fl.x : fl.y, sw = c < 2 ? fl.z : fl.w;
-            R.dl[s] = (unsigned short)((c & 1) ? dw >> 16 : dw & 0xffff);
-            R.sl[s] = (unsigned short)((c & 1) ? sw >> 16 : sw & 0xffff);
+            R.dl[s] = lut_c(B.l[2 * (qi * 3 + s)], c);
+            R.sl[s] = lut_c(B.l[2 * (qi * 3 + s) + 1], c);
         }
     }
 #pragma unroll

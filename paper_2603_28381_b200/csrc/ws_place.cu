@@ -54,7 +54,7 @@ void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     WS_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
-__device__ __forceinline__ unsigned short lut_c(ushort4 v, int c)
+__device__ __forceinline__ int lut_c(int4 v, int c)
 {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(PG_WARPS * 32, 3) k_pg_level(Topo t, LutSrc ls
     // ---- hop 2 / 3 of round 0: root, first in-arc slot, first member slot
     const double sr = act ? C.slew[(size_t)root * 4 + c] : 0.0;
     const double ld = (act && kind == ROOT_ARC) ? C.load[(size_t)root * 4 + c] : 0.0;
-    struct Arc { double v, sf, da; int a; unsigned short dl, sl; };
+    struct Arc { double v, sf, da; int a; int dl, sl; };
     auto load_arc = [&](int qa) {
         Arc r{-INF, 0.0, 0.0, -1, 0, 0};
         if (kind == ROOT_ARC && qa < na) {

@@ -138,3 +138,37 @@ def test_multi_out_arcs_every_mode(name):
         for f in G_FIELDS:
             assert grad_close(dev.get(f), g["gs_" + f]), f
     dev.close()
+
+
+def test_lut_pool_beyond_16_bit_ids():
+    """A design whose every arc owns its tables (the reference's
+    conftest.const_arc style: LUTs deduplicated by object identity only):
+    more than 65535 pooled LUTs, same results as the shared-pool design."""
+    from golden_util import load, raw_of
+    g = load("gen_multi_out_50k")
+    raw = raw_of(g)
+    A = raw.n_arcs
+    ids = np.concatenate([raw.arc_dlut, raw.arc_slut], axis=1).reshape(-1)      # 8 per arc
+    assert 8 * A > 65535
+
+    def pack(ptr, flat):
+        lens = np.diff(ptr)[ids]
+        new_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        new_flat = np.concatenate([flat[ptr[i]:ptr[i + 1]] for i in ids])
+        return new_ptr, new_flat
+    kw = {}
+    for ax in ("s", "l", "t"):
+        kw[f"lut_{ax}_ptr"], kw[f"lut_{ax}_flat"] = pack(np.asarray(getattr(raw, f"lut_{ax}_ptr")),
+                                                      np.asarray(getattr(raw, f"lut_{ax}_flat")))
+    own = np.arange(8 * A, dtype=np.int64).reshape(A, 8)
+    big = RawDesign(**{**{f: getattr(raw, f) for f in raw.__dataclass_fields__ if f != "meta"}, **kw,
+                       "arc_dlut": own[:, :4], "arc_slut": own[:, 4:]}).normalized()
+    assert big.n_luts == 8 * A
+    dev = ws.DeviceDesign(big)
+    for flags in MODES.values():
+        dev.run(flags, gamma=float(g["gamma"]))
+        for f in ST_FIELDS:
+            assert np.array_equal(dev.get(f), g["st_" + f]), f
+        for f in G_FIELDS:
+            assert grad_close(dev.get(f), g["g_" + f]), f
+    dev.close()

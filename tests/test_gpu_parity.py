@@ -235,3 +235,27 @@ def test_graph_replay_bit_identical():
         assert np.array_equal(dev.get(f), a[f]), f
     for f in ST_FIELDS:
         assert np.array_equal(a[f], g["st_" + f]), f
+
+
+def test_graph_replay_follows_gamma_and_loss():
+    """The graph cache keys on the pass shape, not on gamma: a placement /
+    annealing loop that changes gamma every call re-uses the executable (its
+    kernel parameters updated in place) and still gets the new gamma's
+    results; more shapes than the cache holds evict the oldest."""
+    from paper_2603_28381_b200 import _lib
+    flat = flat_of("gen_c1_star")
+    dev = flat.dev
+    base = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED
+    g0 = 0.01 * flat.clock_period
+    for i, gamma in enumerate(g0 * np.linspace(0.5, 2.0, 12)):
+        loss = "softplus" if i % 3 == 2 else "hinge"
+        dev.run(base | _lib.RUN_GRAPH, gamma=gamma, loss=loss)
+        got = dev.get("d_arc"), dev.summary()
+        dev.run(base, gamma=gamma, loss=loss)
+        assert np.array_equal(dev.get("d_arc"), got[0]) and dev.summary() == got[1], (i, gamma)
+    for gran in range(1, 20):      # 19 shapes > the 16-entry cache
+        dev.run(base | _lib.RUN_GRAPH, gamma=g0, granularity=gran)
+    dev.run(base, gamma=g0)
+    ref = dev.get("lse_arrival")
+    dev.run(base | _lib.RUN_GRAPH, gamma=g0, granularity=1)
+    assert np.array_equal(dev.get("lse_arrival"), ref)
