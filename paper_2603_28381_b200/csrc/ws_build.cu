@@ -405,6 +405,22 @@ __global__ void k_rc_code(int M, const int* mem_pin, const int* mem_net, const i
     code[f] = net_tree[mem_net[f]] ? -1 : (pin << 1) | (root_net_of_pin[pin] >= 0 ? 1 : 0);
 }
 
+// per-pin code of the pin-order streaming RC: (member << 2) | (pin roots a
+// net) << 1 | 1 for a star-net member, 2 for a root that is no member (its
+// delay and impulse are 0), 0 for pins the kernel skips (tree-net members:
+// k_rc_tree; pins in no net: the free-pin blocks)
+__global__ void k_rc_pcode(int P, const int* member_of_pin, const int* root_net_of_pin,
+                           const int* mem_net, const int* net_tree, int* pcode)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int f = member_of_pin[p], rn = root_net_of_pin[p];
+    int code = 0;
+    if (f >= 0) code = net_tree[mem_net[f]] ? 0 : ((f << 2) | (rn >= 0 ? 2 : 0) | 1);
+    else if (rn >= 0) code = 2;
+    pcode[p] = code;
+}
+
 }  // namespace
 
 
@@ -915,6 +931,12 @@ void build_topology(Context& ctx, const ws_design_desc* d)
     if (M) {
         k_rc_code<<<blocks_for(M), TPB, 0, s>>>(M, t.mem_pin, t.mem_net, t.net_tree,
                                                   t.root_net_of_pin, t.rc_code);
+        WS_CHECK_LAUNCH();
+    }
+    t.rc_pcode = ar.alloc<int>(P);
+    if (P) {
+        k_rc_pcode<<<blocks_for(P), TPB, 0, s>>>(P, t.member_of_pin, t.root_net_of_pin, t.mem_net,
+                                                 t.net_tree, t.rc_pcode);
         WS_CHECK_LAUNCH();
     }
 

@@ -283,6 +283,7 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
             c.lut_global = e && e[0] == '1';
             const char* r = getenv("WS_RC_SCHEME");
             c.rc_cte = r && std::string(r) == "cte";
+            c.rc_pin_order = r && std::string(r) == "pin";
         }
         // blocking streams: with a NULL stream argument the context's work is
         // ordered after (and before) work on the legacy default stream, the

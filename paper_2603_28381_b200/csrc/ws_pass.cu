@@ -641,7 +641,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
                         // exp(+0) = 1: skip the division, whose zero
                         // dividend would take the IEEE slow path
                         const double dx = __dsub_rn(x[k], cm);
-                        z[k] = dx == 0.0 ? 1.0 : exp(__ddiv_rn(dx, g));
+                        z[k] = (k >= R.na || dx == 0.0) ? 1.0 : exp(__ddiv_rn(dx, g));
                     }
                     double rest = 0.0;
 #pragma unroll
@@ -1083,8 +1083,12 @@ __global__ void k_corner_sum(Corner c0, CornerStrides cst, int A, int M, int nc,
 // nets overlap the streaming member blocks (RC 116 -> 108 us at C3).
 constexpr int RC_TPB = 256, RC_ITEMS = 4;
 
+// pin_order: the streaming blocks walk (pin, cond) items instead of
+// (member, cond): the member's res / cap are gathered (32 B per pin) and the
+// pin's load / net_delay / impulse rows are written contiguously (full
+// lines), the non-member roots' zero delay / impulse included.
 __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm, int nbn, int nbf,
-                                                    bool lse)
+                                                    bool lse, bool pin_order)
 {
     pdl_trigger();
     const Corner& C = cs.c[blockIdx.y];
@@ -1097,6 +1101,43 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm,
     // net blocks first: the sequential root-load folds of big nets start
     // early and overlap the streaming member blocks
     const int bx = (int)blockIdx.x < nbn ? (int)blockIdx.x + nbm : (int)blockIdx.x - nbn;
+    if (bx < nbm && pin_order) {
+        const size_t base = (size_t)bx * RC_TPB * RC_ITEMS + threadIdx.x;
+        const size_t n4 = (size_t)t.P * 4;
+        int code[RC_ITEMS];
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            const size_t i = base + (size_t)k * RC_TPB;
+            code[k] = i < n4 ? LDG(t.rc_pcode + (i >> 2)) : 0;
+        }
+        pdl_wait();
+        double b[RC_ITEMS], r[RC_ITEMS];
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            const size_t i = base + (size_t)k * RC_TPB;
+            b[k] = r[k] = 0.0;
+            if (code[k] & 1) {
+                const size_t f = (size_t)(code[k] >> 2) * 4 + (i & 3);
+                b[k] = __ldcs(C.mem_cap + f);
+                r[k] = __ldcs(C.mem_res + f);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RC_ITEMS; k++) {
+            const size_t i = base + (size_t)k * RC_TPB;
+            if (code[k] & 1) {
+                const double d = __dadd_rn(0.0, __dmul_rn(r[k], b[k]));
+                const double rad = __dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, r[k]), b[k]), d), __dmul_rn(d, d));
+                if (!(code[k] & 2)) C.load[i] = b[k];
+                C.net_delay[i] = d;
+                C.impulse[i] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
+            } else if (code[k] == 2) {
+                C.net_delay[i] = 0.0;
+                C.impulse[i] = 0.0;
+            }
+        }
+        return;
+    }
     if (bx < nbm) {
         const size_t base = (size_t)bx * RC_TPB * RC_ITEMS + threadIdx.x;
         const size_t n4 = (size_t)t.M * 4;
@@ -1137,7 +1178,7 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm,
     pdl_wait();
     const double l = root_load8(C.mem_cap + (size_t)s * 4 + c, 4, m);
     C.load[(size_t)root * 4 + c] = __dadd_rn(LDG(C.root_cap + (size_t)n * 4 + c), l);
-    if (!rm) {
+    if (!rm && !pin_order) {
         C.net_delay[(size_t)root * 4 + c] = 0.0;
         C.impulse[(size_t)root * 4 + c] = 0.0;
     }
@@ -2272,14 +2313,17 @@ struct Launcher {
         if (!ctx.t.n_tasks) return false;
         bool took_free = false;
         if (w == 8) {
-            const int nbm = (int)(((size_t)ctx.t.M * 4 + RC_TPB * RC_ITEMS - 1) / (RC_TPB * RC_ITEMS));
+            const bool po = ctx.rc_pin_order;
+            const int nbm = (int)(((size_t)(po ? ctx.t.P : ctx.t.M) * 4 + RC_TPB * RC_ITEMS - 1) /
+                                  (RC_TPB * RC_ITEMS));
             const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
             const int nbf = (with_free && !ctx.rc_cte) ? (ctx.t.n_free + RC_TPB - 1) / RC_TPB : 0;
             took_free = with_free && !ctx.rc_cte;
             if (ctx.rc_cte)
                 launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
             else
-                launch(k_rc_flat, dim3(nbm + nbn + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn, nbf, lse);
+                launch(k_rc_flat, dim3(nbm + nbn + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn, nbf, lse,
+                       po);
             if (ctx.any_tree) {
                 count++;
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);

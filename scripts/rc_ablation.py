@@ -11,7 +11,7 @@ import paper_2603_28381_b200 as ws
 from paper_2603_28381_b200 import _lib, generator as G
 
 raw = G.generate_raw(G.config_c3())
-for scheme in ("flat", "cte"):
+for scheme in (sys.argv[1:] or ["flat", "cte", "pin"]):
     os.environ["WS_RC_SCHEME"] = scheme
     dev = ws.DeviceDesign(raw)
     out = []

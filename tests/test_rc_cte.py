@@ -1,6 +1,8 @@
-"""CTE-scheme RC kernel (the paper's Algorithm 2 ablation, WS_RC_SCHEME=cte):
-bitwise the same RC outputs and pass as the default streaming RC kernel on
-star designs (heavy tail up to 508 members) and on RC-tree designs."""
+"""RC kernel variants — the CTE scheme (the paper's Algorithm 2 ablation,
+WS_RC_SCHEME=cte) and the pin-order streaming kernel (WS_RC_SCHEME=pin):
+bitwise the same RC outputs and pass as the default member-order streaming
+RC kernel on star designs (heavy tail up to 508 members) and on RC-tree
+designs."""
 
 import os
 
@@ -31,9 +33,10 @@ def _run(raw, scheme):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c1tree", "c2"])
-def test_cte_rc_bitwise(cfg):
+@pytest.mark.parametrize("scheme", ["cte", "pin"])
+def test_rc_schemes_bitwise(cfg, scheme):
     raw = G.generate_raw({"c1": G.config_c1(), "c1tree": G.config_c1("random_tree"),
                           "c2": G.config_c2()}[cfg])
-    a, b = _run(raw, "flat"), _run(raw, "cte")
+    a, b = _run(raw, "flat"), _run(raw, scheme)
     for f in FIELDS:
         assert np.array_equal(a[f], b[f]), f
