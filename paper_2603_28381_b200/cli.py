@@ -1,19 +1,22 @@
-"""Command-line surface (the reference's cli.py:65-147
-``gen`` / ``sta`` / ``grad`` with ``--scheme cuda``, over this repo's design
-files).
+"""Command-line surface (the reference's cli.py:43-258
+``gen`` / ``sta`` / ``grad``).
 
-    python -m paper_2603_28381_b200 gen   --config cfg.json --out d.npz
-    python -m paper_2603_28381_b200 sta   --design d.npz [--report r.txt] [--mode fused]
-    python -m paper_2603_28381_b200 grad  --design d.npz [--gamma G] [--loss hinge] [--report r.txt]
+    python -m paper_2603_28381_b200 gen   --config cfg.json --out d.json|d.npz
+    python -m paper_2603_28381_b200 sta   --design d.json|d.npz [--scheme reference|cuda]
+                                          [--report r.txt] [--mode fused]
+    python -m paper_2603_28381_b200 grad  --design d.json|d.npz [--gamma G] [--loss hinge]
+                                          [--check [--strict]] [--fuse] [--report r.txt]
     python -m paper_2603_28381_b200 place --design d.npz [--seed S] [--steps K]
 
-Reports keep the reference's layout (reports.py:44-206): a ``#`` header with
-the design hash, ``key = value`` summary lines, then one row per (pin,
-condition) for timing, or per arc / net edge for gradients, with floats in
-shortest round-trip form.  Pins are named ``p<id>`` (design files carry no
-pin names) and the hash is the ingest file's content hash (ingest.raw_hash)
-rather than the sha256 of the reference's JSON document.  Exit code 0 on
-success, 2 on a bad design file or argument (cli.py:220-222).
+Design files are the reference's JSON document (parse_design /
+serialize_design) or this repo's hash-verified ``.npz`` ingest file.  Every
+pass runs on the device.  ``--scheme reference`` (the default, as in the
+reference) is run_reference's semantics — np.add.reduceat root loads — so the
+timing report of a JSON design is byte-identical to ``stasim sta --scheme
+reference``'s; ``--scheme cuda`` is run_engine's tree-8 pass (the reference's
+engine).  Reports follow reports.py's layout; ``--report`` writes the report
+and a run manifest and prints the summary.  Exit code 0 on success, 1 when a
+requested check fails, 2 on a bad design file or argument (cli.py:220-222).
 """
 
 from __future__ import annotations
@@ -26,18 +29,10 @@ import time
 import numpy as np
 
 from . import __version__
-from .netlist import COND_NAMES
 
-TIMING_FIELDS = ("pin", "condition", "load", "delay", "impulse", "slew", "arrival", "required",
-                 "slack")
-
-
-def _f(x) -> str:
-    return repr(float(x))
-
-
-def _header(kind: str, dhash: str) -> list:
-    return [f"# warpstar-b200 {__version__} {kind} report", f"# design sha256: {dhash}"]
+GRAD_CHECK_THRESHOLD = 1e-4
+_MODES = {"fused": "RUN_FUSED", "persistent": "RUN_PERSISTENT", "streams": "RUN_TWO_STREAM",
+          "sequential": None}
 
 
 def _config_from_doc(doc: dict):
@@ -51,107 +46,128 @@ def _config_from_doc(doc: dict):
     return GeneratorConfig(**doc)
 
 
-def timing_report(raw, dev, mode: str, corner: int = 0) -> str:
-    from . import ingest
-    tns, wns, _ = dev.summary(corner)
-    st = {f: dev.get(f, corner) for f in ("load", "net_delay", "impulse", "slew", "arrival",
-                                         "required", "slack")}
-    lines = _header("timing", raw.meta.get("hash") or ingest.raw_hash(raw))
-    lines.append(f"# scheme: cuda ({mode})")
-    lines += [f"tns = {_f(tns)}", f"wns = {_f(wns)}", f"level_count = {dev.n_levels}",
-              f"pins = {dev.n_pins}", f"nets = {dev.n_nets}", "", " ".join(TIMING_FIELDS)]
-    cols = [st[f] for f in ("load", "net_delay", "impulse", "slew", "arrival", "required", "slack")]
-    for p in range(dev.n_pins):
-        for c in range(4):
-            lines.append(" ".join([f"p{p}", COND_NAMES[c]] + [_f(a[p, c]) for a in cols]))
-    return "\n".join(lines) + "\n"
+def _write(path, text):
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(text)
 
 
-def gradient_report(raw, dev, gamma: float, loss_kind: str, corner: int = 0) -> str:
-    from . import ingest
-    _, _, loss = dev.summary(corner)
-    d_arc, d_edge = dev.get("d_arc", corner), dev.get("d_edge", corner)
-    arc_delay, nd = dev.get("arc_delay", corner), dev.get("net_delay", corner)
-    lines = _header("gradient", raw.meta.get("hash") or ingest.raw_hash(raw))
-    lines += [f"loss = {_f(loss)}", f"gamma = {_f(gamma)}", f"loss_kind = {loss_kind}"]
-    best = ("none", -1, "", 0.0)
-    if d_arc.size:
-        a, j = divmod(int(np.abs(d_arc).argmax()), 2)
-        best = ("arc", a, ("late-rise", "late-fall")[j], float(d_arc[a, j]))
-    if d_edge.size:
-        k, j = divmod(int(np.abs(d_edge).argmax()), 2)
-        if abs(d_edge[k, j]) > abs(best[3]):
-            best = ("edge", k, ("late-rise", "late-fall")[j], float(d_edge[k, j]))
-    lines.append(f"max_grad_coordinate = {best[0]}:{best[1]}:{best[2]} value {_f(best[3])}")
-    lines += ["", "id from to delay_late_rise delay_late_fall grad_late_rise grad_late_fall"]
-    for a in range(len(raw.arc_from)):
-        lines.append(" ".join([f"arc:{a}", f"p{raw.arc_from[a]}", f"p{raw.arc_to[a]}",
-                               _f(arc_delay[a, 2]), _f(arc_delay[a, 3]), _f(d_arc[a, 0]),
-                               _f(d_arc[a, 1])]))
-    par = np.asarray(raw.mem_parent_pin)
-    root = np.repeat(np.asarray(raw.net_root), np.diff(np.asarray(raw.net_mptr)))
-    for k in range(len(raw.mem_pin)):
-        pin, pp = int(raw.mem_pin[k]), int(par[k])
-        if pp == root[k]:
-            dl = (nd[pin, 2], nd[pin, 3])
-        else:
-            dl = (nd[pin, 2] - nd[pp, 2], nd[pin, 3] - nd[pp, 3])
-        lines.append(" ".join([f"edge:{k}", f"p{pp}", f"p{pin}", _f(dl[0]), _f(dl[1]),
-                               _f(d_edge[k, 0]), _f(d_edge[k, 1])]))
-    return "\n".join(lines) + "\n"
+def _load(path):
+    """(design object or RawDesign, design hash) of a JSON document or an
+    ingest file."""
+    from . import ingest, reports
+    from .design_io import parse_design
+    if path.endswith(".npz"):
+        raw = ingest.load_raw(path)
+        return raw, raw.meta.get("hash") or ingest.raw_hash(raw)
+    with open(path, "r", encoding="utf-8") as fh:
+        text = fh.read()
+    return parse_design(text), reports.design_hash(text)
 
 
-def _write_or_print(path, text):
-    if path:
-        with open(path, "w", encoding="utf-8") as fh:
-            fh.write(text)
-    else:
-        sys.stdout.write(text)
+def _flat(design):
+    from .flatten import flatten
+    return flatten(design)
+
+
+def _state(flat, scheme, mode):
+    """The timing state of the pass the scheme names."""
+    from . import _lib
+    from .sta import TimingState, run_reference
+    if scheme == "reference":
+        return run_reference(flat)
+    dev = flat.dev
+    flags = _lib.RUN_HARD | (getattr(_lib, _MODES[mode]) if _MODES[mode] else 0)
+    if mode != "sequential":
+        flags |= _lib.RUN_LSE | _lib.RUN_GRAD
+    dev.run(flags)
+    return TimingState.from_device(dev, 0, n_levels=flat.n_levels)
 
 
 def cmd_gen(args) -> int:
-    from . import ingest
-    from .generator import generate_raw
+    from . import ingest, reports
+    from .generator import generate_design, generate_raw
+    t0 = time.perf_counter()
     with open(args.config, "r", encoding="utf-8") as fh:
         cfg = _config_from_doc(json.load(fh))
-    raw = generate_raw(cfg)
-    h = ingest.save_raw(args.out, raw)
-    print(f"#Cells {cfg.num_cells}  #Nets {raw.n_nets}  #Pins {raw.n_pins}  sha256 {h}")
+    if args.out.endswith(".npz"):
+        raw = generate_raw(cfg)
+        dhash = ingest.save_raw(args.out, raw)
+        n_nets, n_pins = raw.n_nets, raw.n_pins
+    else:
+        from .design_io import serialize_design
+        d = generate_design(cfg)
+        text = serialize_design(d)
+        _write(args.out, text)
+        dhash, n_nets, n_pins = reports.design_hash(text), len(d.nets), d.n_pins
+    _write(args.out + ".manifest.json",
+           reports.run_manifest("gen", cfg.to_doc(), dhash, cfg.seed, [args.out], time.perf_counter() - t0))
+    print(f"#Cells {cfg.num_cells}  #Nets {n_nets}  #Pins {n_pins}")
     return 0
 
 
-_MODES = {"fused": "RUN_FUSED", "persistent": "RUN_PERSISTENT", "streams": "RUN_TWO_STREAM",
-          "sequential": None}
-
-
-def _run(args, grad: bool):
-    from . import _lib, ingest
-    from .engine import DeviceDesign
-    raw = ingest.load_raw(args.design)
-    dev = DeviceDesign(raw)
-    flags = _lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD
-    if _MODES[args.mode]:
-        flags |= getattr(_lib, _MODES[args.mode])
-    t0 = time.perf_counter()
-    gamma = dev.run(flags, gamma=getattr(args, "gamma", None), loss=getattr(args, "loss", "hinge"))
-    dev.sync()
-    print(f"# {args.mode} pass: {1e3 * (time.perf_counter() - t0):.3f} ms (host wall, first call)",
-          file=sys.stderr)
-    return raw, dev, gamma
-
-
 def cmd_sta(args) -> int:
-    raw, dev, _ = _run(args, False)
-    _write_or_print(args.report, timing_report(raw, dev, args.mode))
-    dev.close()
+    from . import reports
+    t0 = time.perf_counter()
+    design, dhash = _load(args.design)
+    flat = _flat(design)
+    state = _state(flat, args.scheme, args.mode)
+    text = reports.timing_report(flat, state, args.scheme, dhash=dhash)
+    if args.report:
+        _write(args.report, text)
+        _write(args.report + ".manifest.json",
+               reports.run_manifest("sta", {"design": args.design, "scheme": args.scheme}, dhash,
+                                    None, [args.report], time.perf_counter() - t0))
+        for k, v in reports.timing_summary(flat, state).items():
+            print(f"{k} = {v}")
+    else:
+        sys.stdout.write(text)
     return 0
 
 
 def cmd_grad(args) -> int:
-    raw, dev, gamma = _run(args, True)
-    _write_or_print(args.report, gradient_report(raw, dev, gamma, args.loss))
-    dev.close()
-    return 0
+    from . import reports
+    from .diff import LseConfig, default_gamma, finite_diff_check, timing_gradients
+    if args.gamma is not None and not args.gamma > 0:
+        print("warpstar-b200: error: --gamma must be > 0", file=sys.stderr)
+        return 2
+    if args.strict and not args.check:
+        print("warpstar-b200: error: --strict requires --check", file=sys.stderr)
+        return 2
+    design, dhash = _load(args.design)
+    flat = _flat(design)
+    state = _state(flat, args.scheme, "fused")
+    gamma = args.gamma if args.gamma is not None else default_gamma(flat.clock_period)
+    cfg = LseConfig(gamma)
+    gstate = timing_gradients(flat, cfg=cfg, loss=args.loss, state=state)
+    fd = finite_diff_check(flat, cfg=cfg, loss=args.loss) if args.check else None
+    text = reports.gradient_report(flat, state, gstate, fd, dhash=dhash)
+    rc = 0
+    if args.fuse:
+        from .fusion import FusionConfig, execute_fused, execute_sequential
+        fcfg = FusionConfig(granularity=args.granularity, gamma=gamma, loss=args.loss)
+        st_s, gs_s, seq = execute_sequential(flat, cfg=fcfg)
+        st_f, gs_f, fus = execute_fused(flat, cfg=FusionConfig(granularity=args.granularity, gamma=gamma,
+                                                               loss=args.loss, mode="streams"))
+        text += "\n" + reports.fusion_summary(dhash, seq, fus)
+        same = (all(np.array_equal(getattr(st_s, f), getattr(st_f, f), equal_nan=True)
+                    for f in ("load", "net_delay", "impulse", "slew", "arrival", "required", "slack",
+                              "arc_delay")) and gs_s.values_equal(gs_f))
+        if not same:
+            print("warpstar-b200: fused pipeline values differ from sequential", file=sys.stderr)
+            rc = 1
+    if args.report:
+        _write(args.report, text)
+        _write(args.report + ".manifest.json",
+               reports.run_manifest("grad", {"design": args.design, "gamma": gamma, "loss": args.loss},
+                                    dhash, None, [args.report], None))
+        print(f"loss = {gstate.loss!r}")
+    else:
+        sys.stdout.write(text)
+    if args.check and args.strict and fd.max_rel_error > GRAD_CHECK_THRESHOLD:
+        print(f"warpstar-b200: finite-difference max rel error {fd.max_rel_error:.3e} exceeds "
+              f"{GRAD_CHECK_THRESHOLD:.0e}", file=sys.stderr)
+        rc = 1
+    return rc
 
 
 def cmd_place(args) -> int:
@@ -162,11 +178,12 @@ def cmd_place(args) -> int:
     dev = DeviceDesign(raw)
     timer = placement.PlacementTimer(dev, pl, loss=args.loss)
     rng = np.random.default_rng(args.seed)
+    f = lambda x: repr(float(x))
     for t in range(args.steps):
         xy = pl.xy + args.sigma * rng.standard_normal(pl.cell_xy.shape)[pl.cell_of_pin] * (t > 0)
         tns, wns, loss = timer.step(xy)
         g = timer.grad_xy()
-        print(f"step {t}: loss {_f(loss)} tns {_f(tns)} wns {_f(wns)} max|dL/dxy| {_f(np.abs(g).max())}")
+        print(f"step {t}: loss {f(loss)} tns {f(tns)} wns {f(wns)} max|dL/dxy| {f(np.abs(g).max())}")
     dev.close()
     return 0
 
@@ -174,20 +191,27 @@ def cmd_place(args) -> int:
 def build_parser():
     p = argparse.ArgumentParser(prog="python -m paper_2603_28381_b200",
                                 description="B200 differentiable STA (Warp-STAR hot path)")
-    p.add_argument("--version", action="version", version=__version__)
+    p.add_argument("--version", action="version", version=f"stasim {__version__} (warpstar-b200)")
     sub = p.add_subparsers(dest="cmd", required=True)
-    g = sub.add_parser("gen", help="generate a synthetic design file")
+    g = sub.add_parser("gen", help="generate a synthetic design (JSON document or .npz)")
     g.add_argument("--config", required=True, help="GeneratorConfig JSON")
-    g.add_argument("--out", required=True, help="design file (.npz)")
+    g.add_argument("--out", required=True, help="design file (.json or .npz)")
     g.set_defaults(func=cmd_gen)
     for name, func, help_ in (("sta", cmd_sta, "timing report"), ("grad", cmd_grad, "gradient report")):
         s = sub.add_parser(name, help=help_)
         s.add_argument("--design", required=True)
-        s.add_argument("--report", default=None, help="output file (default stdout)")
-        s.add_argument("--mode", default="fused", choices=tuple(_MODES))
-        if name == "grad":
+        s.add_argument("--scheme", default="reference", choices=("reference", "cuda"),
+                       help="reference: run_reference semantics; cuda: the tree-8 engine pass")
+        s.add_argument("--report", default=None, help="output file (stdout then carries the summary)")
+        if name == "sta":
+            s.add_argument("--mode", default="fused", choices=tuple(_MODES))
+        else:
             s.add_argument("--gamma", type=float, default=None)
             s.add_argument("--loss", default="hinge", choices=("hinge", "softplus"))
+            s.add_argument("--check", action="store_true", help="finite-difference gradient check")
+            s.add_argument("--strict", action="store_true", help="with --check: exit 1 above 1e-4")
+            s.add_argument("--fuse", action="store_true", help="sequential vs two-stream pipeline")
+            s.add_argument("--granularity", type=int, default=10)
         s.set_defaults(func=func)
     s = sub.add_parser("place", help="placement steps with position gradients")
     s.add_argument("--design", required=True)

@@ -347,9 +347,34 @@ def generate_raw(cfg: GeneratorConfig) -> RawDesign:
     ).normalized()
 
 
+def _pin_names(raw: RawDesign, n_cells: int) -> list:
+    """The reference generator's pin names (generator.py:240-309): cell
+    output ``c{cell}/o`` (pins 0..n_cells-1), the cell's k-th input
+    ``c{cell}/i{k}`` (its k-th arc, in creation order), endpoint pins
+    ``ep{j}`` in creation (= id) order."""
+    names = [f"c{c}/o" for c in range(n_cells)] + [""] * (raw.n_pins - n_cells)
+    to = np.asarray(raw.arc_to, dtype=np.int64)
+    fr = np.asarray(raw.arc_from, dtype=np.int64)
+    if len(to):
+        first = np.concatenate([[0], np.flatnonzero(to[1:] != to[:-1]) + 1])
+        k = np.arange(len(to)) - np.repeat(first, np.diff(np.concatenate([first, [len(to)]])))
+        for p, c, kk in zip(fr.tolist(), to.tolist(), k.tolist()):
+            names[p] = f"c{c}/i{kk}"
+    j = 0
+    for p in range(n_cells, raw.n_pins):
+        if not names[p]:
+            names[p] = f"ep{j}"
+            j += 1
+    return names
+
+
 def generate_design(cfg: GeneratorConfig):
-    """Object-model design (API convenience over :func:`generate_raw`)."""
-    return raw_to_design(generate_raw(cfg))
+    """Object-model design (API convenience over :func:`generate_raw`), with
+    the reference generator's pin names."""
+    raw = generate_raw(cfg)
+    d = raw_to_design(raw)
+    d.pin_names = _pin_names(raw, cfg.num_cells)
+    return d
 
 
 # BASELINE.md §2 workloads
