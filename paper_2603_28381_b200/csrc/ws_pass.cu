@@ -710,7 +710,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
         }
         if (LSE && late) C.lse_at[pin * 2 + j] = __dadd_rn(S.lr[mq * 2 + j], nd);
     }
-    __syncthreads();                         // smem reusable by the next task
+    if (STATIC) __syncthreads();             // (persistent kernel) smem reusable by the next task
 }
 
 // ---- backward level (backward_level, _kernels.pyx:213-249) + reverse adjoint
@@ -1045,7 +1045,7 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
             }
         }
     }
-    __syncthreads();                         // smem reusable by the next task
+    if (STATIC) __syncthreads();             // (persistent kernel) smem reusable by the next task
 }
 
 // sum over the corners of a batch, in corner order (WS_RUN_CORNER_SUM): the
