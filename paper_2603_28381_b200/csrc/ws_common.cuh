@@ -114,7 +114,13 @@ constexpr int TQ_KIND = 3, TQ_ROOT_MEMBER = 4, TQ_TREE = 8, TQ_ROOT_EP = 16, TQ_
 constexpr int TM_ROOT = 1, TM_EP = 2, TM_MULTI_EP = 4;
 // task limits: a 256-thread block holds one (net, cond) item and ITEMS
 // (arc, cond) / (member, cond) items per thread
-constexpr int PASS_TPB = 256, ITEMS = 2;
+#ifndef WS_TPB
+#define WS_TPB 256
+#endif
+#ifndef WS_ITEMS
+#define WS_ITEMS 2
+#endif
+constexpr int PASS_TPB = WS_TPB, ITEMS = WS_ITEMS;
 constexpr int TASK_Q = PASS_TPB / 4, TASK_A = ITEMS * PASS_TPB / 4, TASK_M = ITEMS * PASS_TPB / 4;
 // task flags: CHUNK = one chunk of a big star net's members; WIDE = one net
 // with more than TASK_A in-arcs; LOOP = one tree net with more than TASK_M
@@ -163,6 +169,10 @@ __host__ __device__ __forceinline__ Corner corner_at(const Corner& c, const Corn
     if (r.mem_buf) { r.mem_buf += kk * s.M4; r.mem_dbuf += kk * s.M4; }   // tree-net scratch
     return r;
 }
+
+// component c of an int4 LUT-id record read as one 32-bit word: a register
+// select of a loaded int4 compiles to four predicated scalar loads per id
+__device__ __forceinline__ int lut_id(const int4* rec, int c) { return reinterpret_cast<const int*>(rec)[c]; }
 
 struct LutView {
     const int *s_ptr, *l_ptr, *t_ptr;
@@ -351,6 +361,15 @@ __host__ __device__ inline size_t lut_smem_bytes(int nl, int s_len, int l_len, i
     return ints * 4 + (size_t)nl * 16 + (size_t)(s_len + l_len + t_len) * 8;
 }
 
+// the pool read in place through L1 (read-only for the whole pass)
+__device__ __forceinline__ LutView lut_view_global(const LutSrc& src, const double* t_flat)
+{
+    LutView v;
+    v.s_ptr = src.s_ptr; v.l_ptr = src.l_ptr; v.t_ptr = src.t_ptr;
+    v.s = src.s; v.l = src.l; v.t = t_flat; v.info = src.info;
+    return v;
+}
+
 // Copies the pool (axes + this corner's tables) into smem when it fits
 // (use_smem), else views global memory.  Ends with __syncthreads unless
 // `sync` is false (the caller then owns the barrier before first use).
@@ -380,6 +399,49 @@ __device__ __forceinline__ LutView stage_luts(const LutSrc& src, const double* t
     for (int i = threadIdx.x; i < src.l_len; i += blockDim.x) dp[src.s_len + i] = src.l[i];
     for (int i = threadIdx.x; i < src.t_len; i += blockDim.x) dp[src.s_len + src.l_len + i] = t_flat[i];
     if (sync) __syncthreads();
+    v.s_ptr = ip; v.l_ptr = ip + n1; v.t_ptr = ip + 2 * n1;
+    v.s = dp; v.l = dp + src.s_len; v.t = dp + src.s_len + src.l_len;
+    v.info = inf;
+    return v;
+}
+
+// The same staging by cp.async (no thread waits on the pool's loads, so a
+// kernel prologue's record loads are not serialized behind it).  The caller
+// must cp.async.wait_all + __syncthreads before the first use.
+__device__ __forceinline__ void cpa_(void* dst, const void* src, int bytes)
+{
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    if (bytes == 16) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ LutView stage_luts_async(const LutSrc& src, const double* t_flat, bool use_smem,
+                                                    unsigned char* smem)
+{
+    LutView v;
+    if (!use_smem) {
+        v.s_ptr = src.s_ptr; v.l_ptr = src.l_ptr; v.t_ptr = src.t_ptr;
+        v.s = src.s; v.l = src.l; v.t = t_flat; v.info = src.info;
+        return v;
+    }
+    const int n1 = src.nl + 1;
+    int* ip = reinterpret_cast<int*>(smem);
+    size_t ints = 3 * (size_t)n1;
+    ints = (ints + 3) & ~(size_t)3;
+    int4* inf = reinterpret_cast<int4*>(smem + ints * 4);
+    double* dp = reinterpret_cast<double*>(smem + ints * 4 + (size_t)src.nl * 16);
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+        cpa_(ip + i, src.s_ptr + i, 4);
+        cpa_(ip + n1 + i, src.l_ptr + i, 4);
+        cpa_(ip + 2 * n1 + i, src.t_ptr + i, 4);
+    }
+    if (src.info)
+        for (int i = threadIdx.x; i < src.nl; i += blockDim.x) cpa_(inf + i, src.info + i, 16);
+    for (int i = threadIdx.x; i < src.s_len; i += blockDim.x) cpa_(dp + i, src.s + i, 8);
+    for (int i = threadIdx.x; i < src.l_len; i += blockDim.x) cpa_(dp + src.s_len + i, src.l + i, 8);
+    for (int i = threadIdx.x; i < src.t_len; i += blockDim.x) cpa_(dp + src.s_len + src.l_len + i, t_flat + i, 8);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     v.s_ptr = ip; v.l_ptr = ip + n1; v.t_ptr = ip + 2 * n1;
     v.s = dp; v.l = dp + src.s_len; v.t = dp + src.s_len + src.l_len;
     v.info = inf;

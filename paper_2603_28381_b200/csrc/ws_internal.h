@@ -112,6 +112,14 @@ struct PgArgs {
     PlaceCorner g;
 };
 
+// read-only device view of the sweep's topology extras (PlaceTopo minus the
+// host vector) and the per-corner {engine, placement} pointer table
+struct PgDev {
+    const int* tm_f;      // [M] task-order member slot -> original member index
+    const int* tm_root;   // [M] task-order member slot -> root pin of its net
+    const PgArgs* pa;     // per corner of the launch (blockIdx.y)
+};
+
 struct CornerSlot {
     Corner d;                  // device pointers
     bool has_lse = false;      // LSE forward done since the last hard pass
@@ -180,6 +188,12 @@ int launch_wire(Context& ctx, int c0, int nc, cudaStream_t s);
 // `gs` and level l starts as soon as the pass's backward level l is done
 int launch_posgrad(Context& ctx, int c0, int nc, cudaStream_t s, cudaStream_t gs = nullptr,
                    const std::vector<cudaEvent_t>* bwd_done = nullptr);
+// the fused mode's pieces of the sweep: gsa / gsr reset before the backward
+// levels (which run the per-level sweep inside k_bwd), then dL/dlength and
+// dL/dxy after them
+PgDev pg_dev(const Context& ctx, int c0);
+void posgrad_reset(Context& ctx, int c0, int nc, cudaStream_t s);
+int launch_posgrad_tail(Context& ctx, int c0, int nc, cudaStream_t s, bool pdl);
 void summary_plan_init(Context& ctx);
 void summary_plan_free(Context& ctx);
 void topo_field_to_host(Context& ctx, int field, int64_t* dst);

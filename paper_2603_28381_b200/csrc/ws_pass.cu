@@ -32,10 +32,15 @@
 #include <curand_kernel.h>
 #include <math.h>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "ws_internal.h"
+#include "ws_pg.cuh"
 
 namespace ws {
 
@@ -98,10 +103,6 @@ __device__ double seed_multi(const Topo& t, const Corner& C, int pin, int j, dou
     return a;
 }
 
-__device__ __forceinline__ int lut_c(int4 v, int c)
-{
-    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
-}
 
 // Programmatic dependent launch (sm_90+): every pass kernel lets the next
 // kernel in the stream start launching immediately, runs its static prologue
@@ -288,6 +289,26 @@ __device__ __forceinline__ bool last_chunk(unsigned* ctr, int nch, int* s_flag)
 
 #define LDG(p) __ldcg(p)
 
+#ifdef WS_PROBE
+// per-launch block timeline: 0 start | 1 records loaded | 2 PDL wait released | 3 end | 4 SM id
+// | 5-7 phases of the fused position-gradient backward level
+#define LSTAMP(slot)                                                                          \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && t.probe) {                                                    \
+            unsigned long long _v;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
+            t.probe[(size_t)blockIdx.x * 8 + (slot)] = _v;                                     \
+            if ((slot) == 0) {                                                                \
+                unsigned _sm;                                                                 \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(_sm));                              \
+                t.probe[(size_t)blockIdx.x * 8 + 4] = _sm;                                    \
+            }                                                                                 \
+        }                                                                                     \
+    } while (0)
+#else
+#define LSTAMP(slot) do { } while (0)
+#endif
+
 // WS_PROBE builds: phase stamps inside task bodies of the persistent kernel
 // (plev >= 0), laid out after the per-level stamps
 #ifdef WS_PROBE
@@ -445,8 +466,8 @@ __device__ __forceinline__ void fwd_records(const Topo& t, const Task& T, FwdSme
                     R.from[k] = t.ta_from[qa];
                     R.arc[k] = t.ta_arc[qa];
                     if (HARD) {
-                        R.dl[k] = lut_c(t.ta_lut[2 * (size_t)qa], c);
-                        R.sl[k] = lut_c(t.ta_lut[2 * (size_t)qa + 1], c);
+                        R.dl[k] = lut_id(t.ta_lut + (2 * (size_t)qa), c);
+                        R.sl[k] = lut_id(t.ta_lut + (2 * (size_t)qa + 1), c);
                     }
                 }
             }
@@ -476,14 +497,14 @@ __device__ void fwd_net_loop(const Topo& t, const LutView& L, const Corner& C, i
         double best = late ? -INF : INF;
         int wq = a0;
         for (int q = a0; q < a1; q++) {
-            const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], c),
+            const double d = lut_interp(L, lut_id(t.ta_lut + (2 * (size_t)q), c),
                                         LDG(C.slew + (size_t)t.ta_from[q] * 4 + c), ld);
             C.arc_delay[(size_t)t.ta_arc[q] * 4 + c] = d;
             const double v = __dadd_rn(LDG(C.arrival + (size_t)t.ta_from[q] * 4 + c), d);
             if (later_wins(late, best, v)) { best = v; wq = q; }
         }
         at = best;
-        sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c), LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), ld);
+        sl = lut_interp(L, lut_id(t.ta_lut + (2 * (size_t)wq + 1), c), LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), ld);
     }
     if (LSE && late) lr = lse_root_global(t, C, a0, a1, c, g, first);
 }
@@ -504,7 +525,7 @@ __device__ void fwd_net_wide(const Topo& t, const LutView& L, const Corner& C, i
             if (later_wins(late, best, v)) { best = v; wq = q; }
         }
         at = best;
-        sl = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)wq + 1], c),
+        sl = lut_interp(L, lut_id(t.ta_lut + (2 * (size_t)wq + 1), c),
                         LDG(C.slew + (size_t)t.ta_from[wq] * 4 + c), LDG(C.load + (size_t)rt * 4 + c));
     }
     if (LSE && late) lr = lse_root_global(t, C, qa0, qa1, c, g, first);
@@ -517,7 +538,7 @@ __device__ void fwd_wide_delays(const Topo& t, const LutView& L, const Corner& C
     for (int i = threadIdx.x; i < T.na * 4; i += blockDim.x) {
         const int q = T.a0 + (i >> 2), cc = i & 3;
         const int fp = t.ta_from[q];
-        const double d = lut_interp(L, lut_c(t.ta_lut[2 * (size_t)q], cc),
+        const double d = lut_interp(L, lut_id(t.ta_lut + (2 * (size_t)q), cc),
                                     LDG(C.slew + (size_t)fp * 4 + cc), LDG(C.load + (size_t)rt * 4 + cc));
         C.arc_delay[(size_t)t.ta_arc[q] * 4 + cc] = d;
     }
@@ -577,6 +598,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
             n_sl = C.pi_slew[(size_t)pi * 4 + c];
         }
     }
+    if (!STATIC) asm volatile("cp.async.wait_all;" ::: "memory");   // the LUT pool (stage_luts_async)
     __syncthreads();                  // net records (and the LUT pool) visible
     BSTAMP(0);
     if (HARD && wide) {
@@ -726,6 +748,85 @@ struct BwdSmem {
     int flag;
 };
 
+// k_bwd<..., PG>: the position-gradient sweep's per-task shared state, in
+// dynamic shared memory after the staged LUT pool.  Late columns only
+// (double2 = conds 2, 3).  The pass-static inputs are prefetched by
+// cp.async in the prologue (before the PDL wait), the sweep-dynamic ones
+// (higher levels' gsa / gsr) right after it, so the sweep step adds no
+// dependent global round trip to the level.
+struct PgSmem {
+    double pt[TASK_M * 2], px[TASK_M * 2], py[TASK_M * 2];   // member terms t, x, y
+    double2 pm[TASK_M * 6];    // slew, impulse, net_delay of the pin; mem_res, mem_cap; root slew
+    double2 pgsa[TASK_M], pgsr[TASK_M];   // gsa of the first out-arc, gsr of the pin
+    int4 pmr[TASK_M];          // pin, first out-arc, tm_flags, original member index
+    double2 pa[TASK_A * 3];    // in-arcs: arrival[from], arc_delay[arc], slew[from]
+    int4 plut[TASK_A];         // delay LUT ids (cond 2, 3), slew LUT ids (cond 2, 3)
+    int aq[TASK_A];            // net of the in-arc within the task
+    double da[TASK_A * 2];     // d_arc of the in-arcs (net phase)
+    double term[TASK_A * 2];   // dL/dload terms of the in-arcs
+    double2 pl[TASK_Q];        // root load
+    double groot[TASK_Q * 2], slw[TASK_Q * 2], wss[TASK_Q * 2];   // root slew adjoint; winner's dS/dload, dS/dslew
+    int win[TASK_Q * 2];       // first strict late max in-arc (-1: none)
+    int2 pop[TASK_Q];          // the root's out-arcs: pin_out_arc[x .. y)
+};
+
+// the prologue prefetch of a task whose nets lie within it (not chunked,
+// looped or wide): records by plain loads, pass state by cp.async.  The
+// first half of the block takes the members, the second the in-arcs and
+// nets, so no thread's copies wait behind another item's record loads.
+__device__ void pg_prefetch_static(const Topo& t, const PgDev& pd, const Corner& C, const Task& T,
+                                   PgSmem& P)
+{
+    constexpr int H = PASS_TPB / 2;
+    if (threadIdx.x < H) {
+        for (int i = threadIdx.x; i < T.nm; i += H) {
+            const int u = T.m0 + i;
+            const int pin = t.tm_pin[u], f = pd.tm_f[u], root = pd.tm_root[u];
+            P.pmr[i] = make_int4(pin, t.tm_o1_arc[u], t.tm_flags[u], f);
+            pg::cp16(&P.pm[i * 6 + 0], C.slew + (size_t)pin * 4 + 2);
+            pg::cp16(&P.pm[i * 6 + 1], C.impulse + (size_t)pin * 4 + 2);
+            pg::cp16(&P.pm[i * 6 + 2], C.net_delay + (size_t)pin * 4 + 2);
+            pg::cp16(&P.pm[i * 6 + 3], C.mem_res + (size_t)f * 4 + 2);
+            pg::cp16(&P.pm[i * 6 + 4], C.mem_cap + (size_t)f * 4 + 2);
+            pg::cp16(&P.pm[i * 6 + 5], C.slew + (size_t)root * 4 + 2);
+        }
+    } else {
+        for (int s = threadIdx.x - H; s < max(T.na, T.nq); s += H) {
+            int root = -1;
+            if (s < T.nq) root = t.tq_root[T.q0 + s];
+            if (s < T.na) {
+                const int qa = T.a0 + s;
+                const int from = t.ta_from[qa], arc = t.ta_arc[qa];
+                const int4 dl = t.ta_lut[2 * (size_t)qa], sl = t.ta_lut[2 * (size_t)qa + 1];
+                P.plut[s] = make_int4(dl.z, dl.w, sl.z, sl.w);
+                P.aq[s] = t.ta_q[qa];
+                pg::cp16(&P.pa[3 * s + 0], C.arrival + (size_t)from * 4 + 2);
+                pg::cp16(&P.pa[3 * s + 1], C.arc_delay + (size_t)arc * 4 + 2);
+                pg::cp16(&P.pa[3 * s + 2], C.slew + (size_t)from * 4 + 2);
+            }
+            if (root >= 0) {
+                pg::cp16(&P.pl[s], C.load + (size_t)root * 4 + 2);
+                P.pop[s] = make_int2(t.pin_out_ptr[root], t.pin_out_ptr[root + 1]);
+            }
+        }
+    }
+    pg::cp_commit();
+}
+
+// after the PDL wait: the higher levels' gsa / gsr (same thread mapping as
+// the static prefetch, so P.pmr[i] is the thread's own write)
+__device__ void pg_prefetch_dyn(const PlaceCorner& G, const Task& T, PgSmem& P)
+{
+    constexpr int H = PASS_TPB / 2;
+    if (threadIdx.x < H)
+    for (int i = threadIdx.x; i < T.nm; i += H) {
+        const int4 r = P.pmr[i];
+        if (r.y >= 0) pg::cp16(&P.pgsa[i], G.gsa + (size_t)r.y * 2);
+        if (r.z & TM_ROOT) pg::cp16(&P.pgsr[i], G.gsr + (size_t)r.x * 2);
+    }
+    pg::cp_commit();
+}
+
 struct BwdRec {
     int pin[ITEMS], fl[ITEMS], o1t[ITEMS], o1a[ITEMS], e1[ITEMS], arc[ITEMS], no[ITEMS], o0[ITEMS];
     int nroot, nflags, ne1;     // this lane's (net, cond) item
@@ -855,9 +956,106 @@ __device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int 
 
 
 
-template <bool HARD, bool GRAD, bool STATIC = false>
+// PG (fused mode with position gradients): the level's position-gradient
+// sweep step (ws_pg.cuh) runs inside the backward level kernel once the
+// members' adjoints and the in-arcs' d_arc are final: member terms after
+// the member phase, the per-net step after the net phase.
+// The net step of the sweep for a task whose nets lie within it, phase-
+// parallel over the task (the arithmetic and order of pg::pg_net_group, so
+// both sweeps agree bit for bit): (net, j) member-term sum, root, winner ->
+// (in-arc, j) LUT partials, gsa, dL/dload terms -> (net, j) dL/dload and
+// (member, j) d_cap.  RC-tree nets run the oracle's recursion.
+__device__ void pg_task_nets(const Topo& t, const LutView& L, const Corner& C, const PlaceCorner& G,
+                             const Task& T, const BwdSmem& S, PgSmem& P)
+{
+    const int tid = threadIdx.x;
+    auto late = [](double2 v, int j) { return j ? v.y : v.x; };
+    for (int i = tid; i < T.nq * 2; i += blockDim.x) {
+        const int ii = i >> 1, j = i & 1;
+        const int fl = S.n.flags[ii], kind = fl & TQ_KIND, root = S.n.root[ii];
+        const int mb = S.n.mptr[ii] - T.m0, m = S.n.mptr[ii + 1] - S.n.mptr[ii];
+        double p0 = 0.0, p1 = 0.0;                // member slots 0, 2, 4, ... / 1, 3, 5, ...
+        for (int k = 0; k < m; k += 2) p0 = __dadd_rn(p0, P.pt[(mb + k) * 2 + j]);
+        for (int k = 1; k < m; k += 2) p1 = __dadd_rn(p1, P.pt[(mb + k) * 2 + j]);
+        const double gsum = __dadd_rn(p0, p1);
+        double groot = gsum;
+        if (kind == ROOT_FEED) {
+            G.gsr[(size_t)root * 2 + j] = gsum;
+        } else {
+            for (int v = P.pop[ii].x; v < P.pop[ii].y; v++)
+                groot = __dadd_rn(groot, __ldcg(G.gsa + (size_t)t.pin_out_arc[v] * 2 + j));
+            G.gs[(size_t)root * 2 + j] = groot;
+        }
+        int w = -1;
+        if (kind == ROOT_ARC) {
+            double best = -INF;
+            const int s0 = S.n.aptr[ii] - T.a0, na = S.n.aptr[ii + 1] - S.n.aptr[ii];
+            for (int k = 0; k < na; k++) {
+                const double v = __dadd_rn(late(P.pa[3 * (s0 + k)], j), late(P.pa[3 * (s0 + k) + 1], j));
+                if (v > best) { best = v; w = k; }
+            }
+            if (w >= 0) {   // the winner's slew-LUT partials (its gsa term and dS/dload)
+                const int sw = s0 + w;
+                double ss, sl;
+                pg::interp_grad(L, j ? P.plut[sw].w : P.plut[sw].z, late(P.pa[3 * sw + 2], j),
+                                late(P.pl[ii], j), ss, sl);
+                P.wss[i] = ss;
+                P.slw[i] = sl;
+            }
+        }
+        P.groot[i] = groot;
+        P.win[i] = w;
+    }
+    __syncthreads();
+    LSTAMP(7);
+    for (int i = tid; i < T.na * 2; i += blockDim.x) {
+        const int s = i >> 1, j = i & 1, ii = P.aq[s];
+        const int4 lu = P.plut[s];
+        const double sf = late(P.pa[3 * s + 2], j), ld = late(P.pl[ii], j), da = P.da[s * 2 + j];
+        double ds, dl;
+        pg::interp_grad(L, j ? lu.y : lu.x, sf, ld, ds, dl);
+        double ga = __dmul_rn(da, ds);
+        P.term[s * 2 + j] = __dmul_rn(da, dl);
+        if (s - (S.n.aptr[ii] - T.a0) == P.win[ii * 2 + j])
+            ga = __dadd_rn(ga, __dmul_rn(P.groot[ii * 2 + j], P.wss[ii * 2 + j]));
+        G.gsa[(size_t)S.arc[s] * 2 + j] = ga;
+    }
+    __syncthreads();
+    // dL/dload of net ii, column j: the in-arc terms in arc order, then the
+    // winner's slew term
+    auto net_gl = [&](int ii, int j) {
+        double gl = 0.0;
+        if ((S.n.flags[ii] & TQ_KIND) == ROOT_ARC) {
+            const int s0 = S.n.aptr[ii] - T.a0, na = S.n.aptr[ii + 1] - S.n.aptr[ii];
+            for (int k = 0; k < na; k++) gl = __dadd_rn(gl, P.term[(s0 + k) * 2 + j]);
+            if (P.win[ii * 2 + j] >= 0) gl = __dadd_rn(gl, __dmul_rn(P.groot[ii * 2 + j], P.slw[ii * 2 + j]));
+        }
+        return gl;
+    };
+    for (int i = tid; i < (T.nq + T.nm) * 2; i += blockDim.x) {
+        const int j = i & 1;
+        if (i < T.nq * 2) {
+            const int ii = i >> 1;
+            const double gl = net_gl(ii, j);
+            const int net = S.n.net[ii];
+            G.gl[(size_t)net * 2 + j] = gl;
+            G.d_root_cap[(size_t)net * 2 + j] = gl;
+            if (S.n.flags[ii] & TQ_TREE)
+                pg::pg_tree_net(t, C, G, S.n.f0[ii], S.n.mptr[ii + 1] - S.n.mptr[ii], j, gl);
+        } else {
+            const int mi = (i >> 1) - T.nq;
+            const int4 r = P.pmr[mi];
+            const int ii = r.z >> 8;
+            if (S.n.flags[ii] & TQ_TREE) continue;
+            G.d_cap[(size_t)r.w * 2 + j] = __dadd_rn(__dadd_rn(P.px[mi * 2 + j], net_gl(ii, j)), P.py[mi * 2 + j]);
+        }
+    }
+}
+
+template <bool HARD, bool GRAD, bool STATIC = false, bool PG = false>
 __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem& S,
-                         const BwdRec& R, double g, int kind, int variant, int plev = -1)
+                         const BwdRec& R, double g, int kind, int variant, int plev = -1,
+                         const LutView* pL = nullptr, const PgDev* ppd = nullptr, PgSmem* pP = nullptr)
 {
     const int tid = threadIdx.x, c = tid & 3, ii = tid >> 2;
     const bool late = c >= 2;
@@ -944,8 +1142,38 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
             S.w[ai * 2 + j] = wgt[k];
             S.arc[ai] = R.arc[k];
         }
+    if (PG) pg::cp_wait_all();               // the sweep's prefetch, published by the barrier
     __syncthreads();
     BSTAMP(1);
+    if (PG) LSTAMP(5);
+    // position-gradient sweep: a task's member terms stay in shared memory
+    // unless the net spans several tasks (chunks) or exceeds them (loop)
+    const bool pg_glob = chunk || loop || wide;
+    if (PG) {   // member terms of the sweep: the members' adjoints are final
+        const PlaceCorner& G = ppd->pa[blockIdx.y].g;
+        PgSmem& P = *pP;
+        for (int i = tid; i < T.nm * 2; i += blockDim.x) {
+            const int u = T.m0 + (i >> 1), jj = i & 1;
+            if (pg_glob) {
+                pg::MemberIn mv = pg::member_load(t, *ppd, C, u, jj);
+                pg::member_load_dyn(G, jj, mv);
+                pg::member_finish(t, G, u, jj, mv, 0, pg::TermsGlobal{&G});
+            } else {
+                const int mi = i >> 1;
+                const int4 r = P.pmr[mi];
+                auto late = [&](double2 v) { return jj ? v.y : v.x; };
+                pg::MemberIn mv;
+                mv.pin = r.x; mv.o1 = r.y; mv.fl = r.z; mv.f = r.w;
+                mv.tree = S.n.flags[r.z >> 8] & TQ_TREE;
+                mv.sm = late(P.pm[mi * 6 + 0]); mv.im = late(P.pm[mi * 6 + 1]);
+                mv.d = late(P.pm[mi * 6 + 2]); mv.rr = late(P.pm[mi * 6 + 3]);
+                mv.cp = late(P.pm[mi * 6 + 4]); mv.sr = late(P.pm[mi * 6 + 5]);
+                mv.adj = S.de[mi * 2 + jj];   // the member phase's adjoint
+                mv.gsa1 = late(P.pgsa[mi]); mv.gsr = late(P.pgsr[mi]);
+                pg::member_finish(t, G, u, jj, mv, mi, pg::TermsSmem{P.pt, P.px, P.py});
+            }
+        }
+    }
     if (chunk) {
         // one chunk of a big star net: ordered partial folds, last chunk combines
         const int nch = t.bn_nch[T.slot];
@@ -990,6 +1218,11 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
             }
         }
         __syncthreads();
+        // the big net's sweep step, once every chunk's member terms are in
+        // (last_chunk fenced them) and its in-arcs' d_arc are written
+        if (PG && last && tid < 32)
+            pg::pg_net_group<4>(t, *pL, C, ppd->pa[blockIdx.y].g, tid < 4 ? T.q0 : -1,
+                                pg::SrcGlobal{{&ppd->pa[blockIdx.y].g}, &t, &C});
         return;
     }
     // ---- net phase: one (net, cond) per thread
@@ -1034,8 +1267,11 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
             C.adjoint[(size_t)rt * 2 + j] = ar;
             if ((fq & TQ_KIND) == ROOT_ARC) {
                 if (!wide) {
-                    for (int q = S.n.aptr[ii] - T.a0; q < S.n.aptr[ii + 1] - T.a0; q++)
-                        C.d_arc[(size_t)S.arc[q] * 2 + j] = __dmul_rn(ar, S.w[q * 2 + j]);
+                    for (int q = S.n.aptr[ii] - T.a0; q < S.n.aptr[ii + 1] - T.a0; q++) {
+                        const double da = __dmul_rn(ar, S.w[q * 2 + j]);
+                        C.d_arc[(size_t)S.arc[q] * 2 + j] = da;
+                        if (PG) pP->da[q * 2 + j] = da;
+                    }
                 } else {
                     for (int q = S.n.aptr[0]; q < S.n.aptr[1]; q++) {
                         const size_t a = (size_t)t.ta_arc[q];
@@ -1044,6 +1280,14 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
                 }
             }
         }
+    }
+    if (PG) {
+        __syncthreads();                     // the in-arcs' d_arc, the member terms
+        LSTAMP(6);
+        const LutView& LG = *pL;
+        const PlaceCorner& G = ppd->pa[blockIdx.y].g;
+        if (pg_glob) pg::pg_net_group<4>(t, LG, C, G, ii < T.nq ? T.q0 + ii : -1, pg::SrcGlobal{{&G}, &t, &C});
+        else pg_task_nets(t, LG, C, G, T, S, *pP);
     }
     if (STATIC) __syncthreads();             // (persistent kernel) smem reusable by the next task
 }
@@ -1273,24 +1517,6 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_tree(Topo t, Corners cs)
 }
 
 // ---- per-level kernels (one task per block; PDL prologue = records) --------
-#ifdef WS_PROBE
-// per-launch block timeline: 0 start | 1 records loaded | 2 PDL wait released | 3 end | 4 SM id
-#define LSTAMP(slot)                                                                          \
-    do {                                                                                      \
-        if (threadIdx.x == 0 && t.probe) {                                                    \
-            unsigned long long _v;                                                            \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_v));                            \
-            t.probe[(size_t)blockIdx.x * 8 + (slot)] = _v;                                     \
-            if ((slot) == 0) {                                                                \
-                unsigned _sm;                                                                 \
-                asm volatile("mov.u32 %0, %%smid;" : "=r"(_sm));                              \
-                t.probe[(size_t)blockIdx.x * 8 + 4] = _sm;                                    \
-            }                                                                                 \
-        }                                                                                     \
-    } while (0)
-#else
-#define LSTAMP(slot) do { } while (0)
-#endif
 
 __global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w, int k0)
 {
@@ -1316,7 +1542,7 @@ __global__ void __launch_bounds__(PASS_TPB, MB) k_fwd(Topo t, LutSrc ls, Corners
     LSTAMP(0);
     const Corner& C = cs.c[blockIdx.y];
     LutView L;
-    if (HARD) L = stage_luts(ls, C.lut_t_flat, use_smem, smem, false);
+    if (HARD) L = stage_luts_async(ls, C.lut_t_flat, use_smem, smem);
     const int k = k0 + blockIdx.x;
     const Task T = load_task(t, k);
     FwdRec R;
@@ -1328,21 +1554,34 @@ __global__ void __launch_bounds__(PASS_TPB, MB) k_fwd(Topo t, LutSrc ls, Corners
     LSTAMP(3);
 }
 
-template <bool HARD, bool GRAD, int MB = WS_MINB>
+template <bool HARD, bool GRAD, int MB = WS_MINB, bool PG = false>
 __global__ void __launch_bounds__(PASS_TPB, MB) k_bwd(Topo t, Corners cs, int k0, double g, int kind,
-                                                     int variant)
+                                                     int variant, LutSrc ls, bool use_smem, PgDev pd,
+                                                     int pg_off)
 {
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ BwdSmem S;
+    // the sweep: the LUT pool staged in the prologue (the member phase's
+    // barrier precedes the first use), its per-task state after it
+    LutView L;
+    PgSmem* P = nullptr;
+    if (PG) {
+        L = stage_luts_async(ls, cs.c[blockIdx.y].lut_t_flat, use_smem, smem);
+        P = reinterpret_cast<PgSmem*>(smem + pg_off);
+    }
     pdl_trigger();
     LSTAMP(0);
     const int k = k0 + blockIdx.x;
     const Task T = load_task(t, k);
     BwdRec R;
     bwd_records<GRAD>(t, T, S, R);
+    const bool pg_pref = PG && !(T.flags & (TK_CHUNK | TK_LOOP | TK_WIDE));
+    if (pg_pref) pg_prefetch_static(t, pd, cs.c[blockIdx.y], T, *P);
     LSTAMP(1);
     pdl_wait();          // the next-higher level's results are now visible
     LSTAMP(2);
-    bwd_body<HARD, GRAD>(t, cs.c[blockIdx.y], T, S, R, g, kind, variant);
+    if (pg_pref) pg_prefetch_dyn(pd.pa[blockIdx.y].g, T, *P);
+    bwd_body<HARD, GRAD, false, PG>(t, cs.c[blockIdx.y], T, S, R, g, kind, variant, -1, &L, &pd, P);
     LSTAMP(3);
 }
 
@@ -1822,8 +2061,8 @@ __device__ __forceinline__ void fwd_records_smem(const FwdBlob& B, const Task& T
         R.from[s] = fa.x;
         R.arc[s] = fa.y;
         if (HARD) {
-            R.dl[s] = lut_c(B.l[2 * (qi * 3 + s)], c);
-            R.sl[s] = lut_c(B.l[2 * (qi * 3 + s) + 1], c);
+            R.dl[s] = lut_id(B.l + (2 * (qi * 3 + s)), c);
+            R.sl[s] = lut_id(B.l + (2 * (qi * 3 + s) + 1), c);
         }
     }
 #pragma unroll
@@ -2264,12 +2503,14 @@ void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStre
 struct Launcher {
     Context& ctx;
     Corners cs;
+    int c0;
     int nc;
+    bool pg = false;     // fused position-gradient sweep inside the backward levels
     int count = 0;
     LutSrc ls;
     size_t lut_bytes;
     bool use_smem;
-    Launcher(Context& c, int c0, int nc_) : ctx(c), nc(nc_)
+    Launcher(Context& c, int c0_, int nc_) : ctx(c), c0(c0_), nc(nc_)
     {
         for (int k = 0; k < nc; k++) cs.c[k] = ctx.corners[c0 + k].d;
         const Topo& t = ctx.t;
@@ -2369,14 +2610,21 @@ struct Launcher {
         const int nt = tasks(li);
         if (nt <= 0) return;
         const int variant = H && G ? 3 : (H ? 1 : 2);
-        if (H && G && nc >= 4)
+        const PgDev pd = pg ? pg_dev(ctx, c0) : PgDev{nullptr, nullptr, nullptr};
+        if (H && G && pg)
+            launch(k_bwd<H, G, WS_MINB, true>, dim3(nt, nc), dim3(PASS_TPB), pg_smem_bytes(), s, probed(nt),
+                   cs, ctx.lvt_ptr_host[li], g, kind, variant, ls, use_smem, pd, pg_off());
+        else if (H && G && nc >= 4)
             launch(k_bwd<H, G, WS_MINB_BATCH>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs,
-                   ctx.lvt_ptr_host[li], g, kind, variant);
+                   ctx.lvt_ptr_host[li], g, kind, variant, ls, false, pd, 0);
         else
             launch(k_bwd<H, G>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs, ctx.lvt_ptr_host[li],
-                   g, kind, variant);
+                   g, kind, variant, ls, false, pd, 0);
         count++;
     }
+    // k_bwd<..., PG>: the staged pool, then the sweep's per-task state
+    int pg_off() const { return (int)((lut_bytes + 15) & ~(size_t)15); }
+    size_t pg_smem_bytes() const { return (size_t)pg_off() + sizeof(PgSmem); }
     // sum_k d_arc / d_edge over the batch
     void corner_sum(cudaStream_t s)
     {
@@ -2479,7 +2727,7 @@ struct Launcher {
 
 void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind, int gran,
                cudaStream_t s, cudaStream_t gs, int w, int& count,
-               const std::vector<cudaEvent_t>* bwd_done = nullptr)
+               const std::vector<cudaEvent_t>* bwd_done = nullptr, bool pg_fused = false)
 {
     const int L = ctx.t.L;
     Launcher la(ctx, c0, nc);
@@ -2489,6 +2737,9 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         WS_CUDA(cudaFuncSetAttribute(k_fwd<true, true, WS_MINB_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)la.lut_bytes));
     }
+    if (pg_fused)   // the staged pool + the sweep's per-task state exceed the default 48 KB
+        WS_CUDA(cudaFuncSetAttribute(k_bwd<true, true, WS_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)la.pg_smem_bytes()));
     const bool hard = flags & WS_RUN_HARD, lse = flags & WS_RUN_LSE, grad = flags & WS_RUN_GRAD;
     const bool fused = (flags & WS_RUN_FUSED) && hard && lse && grad;
     const bool two = (flags & WS_RUN_TWO_STREAM) && hard && (lse || grad) && !fused;
@@ -2510,12 +2761,15 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
             la.fwd<true, true>(s, li, g);
             la.mark(s, 1, li);
         }
+        la.pg = pg_fused;
+        if (pg_fused) posgrad_reset(ctx, c0, nc, s);
         for (int li = L - 1; li >= 0; li--) {
             la.bwd<true, true>(s, li, g, kind);
             if (bwd_done) WS_CUDA(cudaEventRecord((*bwd_done)[li], s));
             la.mark(s, 2, li);
         }
         la.fin_summary(s, g, kind);
+        if (pg_fused) la.count += launch_posgrad_tail(ctx, c0, nc, s, true);
         if (flags & WS_RUN_CORNER_SUM) la.corner_sum(s);
         la.mark(s, 5, -1);
     } else if (two) {
@@ -2641,10 +2895,16 @@ void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int lo
     int count = 0;
     ctx.timed_n = 0;
     if (flags & WS_RUN_WIRE) count += launch_wire(ctx, c0, nc, s);
-    // the position-gradient sweep overlaps the backward sweep on the second
-    // stream (fused single-chunk passes): level l waits only for backward level l
-    const bool overlap = (flags & WS_RUN_POSGRAD) && (flags & WS_RUN_FUSED) && nc <= MAXC &&
-                         !(flags & WS_RUN_PERSISTENT) && ctx.t.L > 0;
+    // fused mode: the position-gradient sweep runs inside the backward level
+    // kernels (k_bwd<..., PG>).  WS_PG_SWEEP=stream keeps the stand-alone
+    // sweep kernels on the second stream instead, level l waiting only for
+    // backward level l (ablation).
+    const bool fused_pass = (flags & WS_RUN_POSGRAD) && (flags & WS_RUN_FUSED) &&
+                            !(flags & WS_RUN_PERSISTENT) && ctx.t.L > 0;
+    const char* sweep_env = getenv("WS_PG_SWEEP");
+    const bool stream_sweep = sweep_env && !strcmp(sweep_env, "stream");
+    const bool pg_fused = fused_pass && !stream_sweep;
+    const bool overlap = fused_pass && stream_sweep && nc <= MAXC;
     std::vector<cudaEvent_t>& ev = ctx.pg_events;
     if (overlap) {
         while ((int)ev.size() < ctx.t.L + 2) {
@@ -2657,8 +2917,8 @@ void run_pass(Context& ctx, int c0, int nc, unsigned flags, double gamma, int lo
     }
     for (int k = 0; k < nc; k += MAXC)
         run_chunk(ctx, c0 + k, std::min(MAXC, nc - k), flags, gamma, loss_kind, granularity, s, gs,
-                  w, count, overlap ? &ev : nullptr);
-    if (flags & WS_RUN_POSGRAD) {
+                  w, count, overlap ? &ev : nullptr, pg_fused);
+    if ((flags & WS_RUN_POSGRAD) && !pg_fused) {
         if (overlap) {
             count += launch_posgrad(ctx, c0, nc, s, gs, &ev);
             WS_CUDA(cudaEventRecord(ev[ctx.t.L + 1], gs));  // join

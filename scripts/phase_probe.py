@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28381_b200 as ws
 from paper_2603_28381_b200 import _lib, generator as G
 
-STRIDE = 8 * 8192 * 4
+STRIDE = 8 * 2048      # Launcher::PROBE_STRIDE: 2048 blocks x 8 stamps per launch
 raw = G.generate_raw(G.config_c3())
 dev = ws.DeviceDesign(raw)
 mode = sys.argv[1] if len(sys.argv) > 1 else "fused"
@@ -38,7 +38,7 @@ for _ in range(2):
     e1.record()
     torch.cuda.synchronize()
 print(f"mode {mode}: pass {e0.elapsed_time(e1):.3f} ms, {dev.last_launch_count()} launches")
-P = probe.view(n_launch, 8192 * 4, 8).cpu().numpy().astype(np.int64)
+P = probe.view(n_launch, 2048, 8).cpu().numpy().astype(np.int64)
 t_all = P[P > 0].min()
 rows = []
 for i in range(n_launch):

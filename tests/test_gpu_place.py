@@ -218,3 +218,42 @@ def test_place_multi_out_arcs(name, loss):
     PL.PlacementTimer(dev, pl, loss=loss).step()
     check(dev, 0, raw, pl, loss)
     dev.close()
+
+
+def _sweep_case(case):
+    if case == "c1":
+        return G.generate_raw(G.config_c1())
+    if case == "tree":
+        return gen(600, "random_tree")
+    if case in ("edge_kinds", "multi_out", "gen_multi_out_tree"):
+        return raw_of(load(case))
+    topo = "star" if case == "big_star" else "random_tree"
+    return G.generate_raw(G.GeneratorConfig(num_cells=2500, fanout=G.power_law(1.1, 300), depth_target=5,
+                                            max_cell_inputs=180, seed=13, net_topology=topo))
+
+
+@pytest.mark.parametrize("case", ["c1", "tree", "edge_kinds", "multi_out", "gen_multi_out_tree",
+                                  "big_star", "big_tree"])
+def test_fused_sweep_equals_stream_sweep(case, monkeypatch):
+    """The fused mode runs the position-gradient sweep inside the backward
+    level kernels (k_bwd<..., PG>); WS_PG_SWEEP=stream runs the stand-alone
+    k_pg_mem / k_pg_level kernels on the second stream.  Same bodies
+    (ws_pg.cuh), same order: bitwise equal, including chunked big star nets
+    (> TASK_M members), TK_WIDE nets and TK_LOOP RC trees; the fused one also
+    matches the oracle."""
+    raw = _sweep_case(case)
+    pl = PL.synthetic_placement(raw, seed=4)
+    out = {}
+    for mode in ("fused", "stream"):
+        if mode == "stream":
+            monkeypatch.setenv("WS_PG_SWEEP", "stream")
+        else:
+            monkeypatch.delenv("WS_PG_SWEEP", raising=False)
+        dev = ws.DeviceDesign(raw)
+        PL.PlacementTimer(dev, pl, graph=mode == "fused").step()
+        out[mode] = {f: dev.get(f) for f, _ in PG_FIELDS}
+        if mode == "fused" and case in ("c1", "big_star", "edge_kinds"):
+            check(dev, 0, raw, pl)
+        dev.close()
+    for f, _ in PG_FIELDS:
+        assert np.array_equal(out["fused"][f], out["stream"][f], equal_nan=True), f
