@@ -649,32 +649,59 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
                     }
                     at = best;
                 }
-                if (LSE && late) {
-                    double x[FWD_NA], z[FWD_NA];
-                    double cm = -INF;
-#pragma unroll
-                    for (int k = 0; k < FWD_NA; k++) {
-                        x[k] = __dadd_rn(xl[k], dd[k]);
-                        if (k < R.na && (k == 0 || x[k] > cm)) cm = x[k];     // np.maximum.reduceat
+                if (LSE) {
+                    // The LSE of the two late columns, spread over the
+                    // net's 4 lanes: column j's owner (lane 2 + j) forms
+                    // x = lse_at[from] + delay and its first max am; of the
+                    // (column, in-arc) exponentials only the <= 4 non-max
+                    // ones are not exactly 1, so lane c takes column c >> 1's
+                    // (c & 1)-th non-max in-arc: one exp per lane instead
+                    // of three on the late lanes.  Same arithmetic as the
+                    // reference order (np.maximum.reduceat, z0 + sequential
+                    // rest, z / s).
+                    const int qb = threadIdx.x & 28;                 // the quad's cond-0 lane
+                    const unsigned qmask = 0xFu << qb;
+                    double x0 = 0.0, x1 = 0.0, x2 = 0.0, cm = -INF;
+                    int am = 0;
+                    if (late) {
+                        x0 = __dadd_rn(xl[0], dd[0]);
+                        x1 = __dadd_rn(xl[1], dd[1]);
+                        x2 = __dadd_rn(xl[2], dd[2]);
+                        cm = x0;                                       // np.maximum.reduceat
+                        if (1 < R.na && x1 > cm) { cm = x1; am = 1; }
+                        if (2 < R.na && x2 > cm) { cm = x2; am = 2; }
                     }
-#pragma unroll
-                    for (int k = 0; k < FWD_NA; k++) {
-                        // the max element gives exactly +0 / g = +0 and
-                        // exp(+0) = 1: skip the division, whose zero
-                        // dividend would take the IEEE slow path
-                        const double dx = __dsub_rn(x[k], cm);
-                        z[k] = (k >= R.na || dx == 0.0) ? 1.0 : exp(__ddiv_rn(dx, g));
+                    const double d0 = __dsub_rn(x0, cm), d1 = __dsub_rn(x1, cm), d2 = __dsub_rn(x2, cm);
+                    const int own = qb + 2 + (c >> 1);                // owner of column c >> 1
+                    const int amj = __shfl_sync(qmask, am, own);
+                    const double dA = __shfl_sync(qmask, am == 0 ? d1 : d0, own);   // first non-max
+                    const double dB = __shfl_sync(qmask, am == 2 ? d1 : d2, own);   // second non-max
+                    const int i1 = c & 1, kk = i1 + (i1 >= amj ? 1 : 0);
+                    const double dm = i1 ? dB : dA;
+                    // the max element's +0 / g = +0 and exp(+0) = 1 need no
+                    // division (whose zero dividend takes the IEEE slow path)
+                    const double e = (kk >= R.na || dm == 0.0) ? 1.0 : exp(__ddiv_rn(dm, g));
+                    const double zA = __shfl_sync(qmask, e, qb + 2 * i1);
+                    const double zB = __shfl_sync(qmask, e, qb + 2 * i1 + 1);
+                    double sc = 1.0;
+                    if (late) {
+                        const double z0 = am == 0 ? 1.0 : zA;
+                        const double z1 = am == 1 ? 1.0 : (am == 0 ? zA : zB);
+                        const double z2 = am == 2 ? 1.0 : zB;
+                        double rest = 0.0;
+                        if (1 < R.na) rest = __dadd_rn(rest, z1);   // reduceat: z0 + sequential (n < 9)
+                        if (2 < R.na) rest = __dadd_rn(rest, z2);
+                        sc = __dadd_rn(z0, rest);
+                        lr = __dadd_rn(cm, __dmul_rn(g, log(sc)));
                     }
-                    double rest = 0.0;
-#pragma unroll
-                    for (int k = 1; k < FWD_NA; k++)
-                        if (k < R.na) rest = __dadd_rn(rest, z[k]);   // reduceat: z0 + sequential (n < 9)
-                    const double s = __dadd_rn(z[0], rest);
-                    lr = __dadd_rn(cm, __dmul_rn(g, log(s)));
-                    if (first)
-#pragma unroll
-                        for (int k = 0; k < FWD_NA; k++)
-                            if (k < R.na) C.weights[(size_t)R.arc[k] * 2 + j] = __ddiv_rn(z[k], s);
+                    const double sj = __shfl_sync(qmask, sc, own);
+                    if (first) {
+                        // weights z / s: each lane its non-max in-arc of column
+                        // c >> 1, the owner also its column's max (z = 1)
+                        auto arc_of = [&](int k) { return k == 0 ? R.arc[0] : (k == 1 ? R.arc[1] : R.arc[2]); };
+                        if (kk < R.na) C.weights[(size_t)arc_of(kk) * 2 + (c >> 1)] = __ddiv_rn(e, sj);
+                        if (late) C.weights[(size_t)arc_of(am) * 2 + j] = __ddiv_rn(1.0, sc);
+                    }
                 }
             }
             if (first) {
