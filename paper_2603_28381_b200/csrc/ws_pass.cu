@@ -544,6 +544,136 @@ __device__ void fwd_wide_delays(const Topo& t, const LutView& L, const Corner& C
     }
 }
 
+// The (net, cond) item of a forward level: in-arcs of the net in arc order
+// (first arc wins ties), the winner's output slew, the LSE of the late
+// columns; writes the arc delays, weights and the root's arrival / slew /
+// lse (when `first`).  The LSE shuffles need the net's four cond lanes
+// together in one quad.
+template <bool HARD, bool LSE>
+__device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, const Corner& C, const FwdRec& R,
+                                             int kind, int rt, bool wide, int wa0, int wa1, bool first,
+                                             const double* slf, const double* atf, const double* xl, double* dd,
+                                             double ld, double n_at, double n_sl, double n_lr, int c, double g,
+                                             double& at, double& sl, double& lr)
+{
+    const bool late = c >= 2;
+    const int j = c - 2;
+    if (kind == ROOT_ARC) {
+        if (wide) {
+            fwd_net_wide<HARD, LSE>(t, L, C, wa0, wa1, rt, c, g, first, at, sl, lr);
+        } else if (R.na > FWD_NA) {
+            fwd_net_loop<HARD, LSE>(t, L, C, R.a0, R.a0 + R.na, rt, ld, c, g, first, at, sl, lr);
+        } else {
+            if (HARD) {
+                // every slot's delay and output slew (independent chains),
+                // then the ordered merge; the root load is located once
+                // on the first arc's load axis
+                const int4 d0 = L.info[R.dl[0]];
+                const Loc ll0 = lut_locate(L.l + d0.z, d0.w, ld);
+                double sw[FWD_NA];
+#pragma unroll
+                for (int k = 0; k < FWD_NA; k++) {
+                    const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
+                    const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
+                    const Loc lld = (di.z == d0.z && di.w == d0.w) ? ll0 : lut_locate(L.l + di.z, di.w, ld);
+                    dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
+                    const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
+                    const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld);
+                    sw[k] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
+                }
+                double best = late ? -INF : INF;
+                sl = sw[0];
+#pragma unroll
+                for (int k = 0; k < FWD_NA; k++) {
+                    if (k >= R.na) break;
+                    C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
+                    const double v = __dadd_rn(atf[k], dd[k]);
+                    if (later_wins(late, best, v)) { best = v; sl = sw[k]; }
+                }
+                at = best;
+            }
+            if (LSE) {
+                // The LSE of the two late columns, spread over the
+                // net's 4 lanes: column j's owner (lane 2 + j) forms
+                // x = lse_at[from] + delay and its first max am; of the
+                // (column, in-arc) exponentials only the <= 4 non-max
+                // ones are not exactly 1, so lane c takes column c >> 1's
+                // (c & 1)-th non-max in-arc: one exp per lane instead
+                // of three on the late lanes.  Same arithmetic as the
+                // reference order (np.maximum.reduceat, z0 + sequential
+                // rest, z / s).
+                const int qb = threadIdx.x & 28;                 // the quad's cond-0 lane
+                const unsigned qmask = 0xFu << qb;
+                double x0 = 0.0, x1 = 0.0, x2 = 0.0, cm = -INF;
+                int am = 0;
+                if (late) {
+                    x0 = __dadd_rn(xl[0], dd[0]);
+                    x1 = __dadd_rn(xl[1], dd[1]);
+                    x2 = __dadd_rn(xl[2], dd[2]);
+                    cm = x0;                                       // np.maximum.reduceat
+                    if (1 < R.na && x1 > cm) { cm = x1; am = 1; }
+                    if (2 < R.na && x2 > cm) { cm = x2; am = 2; }
+                }
+                const double d0 = __dsub_rn(x0, cm), d1 = __dsub_rn(x1, cm), d2 = __dsub_rn(x2, cm);
+                const int own = qb + 2 + (c >> 1);                // owner of column c >> 1
+                const int amj = __shfl_sync(qmask, am, own);
+                const double dA = __shfl_sync(qmask, am == 0 ? d1 : d0, own);   // first non-max
+                const double dB = __shfl_sync(qmask, am == 2 ? d1 : d2, own);   // second non-max
+                const int i1 = c & 1, kk = i1 + (i1 >= amj ? 1 : 0);
+                const double dm = i1 ? dB : dA;
+                // the max element's +0 / g = +0 and exp(+0) = 1 need no
+                // division (whose zero dividend takes the IEEE slow path)
+                const double e = (kk >= R.na || dm == 0.0) ? 1.0 : exp(__ddiv_rn(dm, g));
+                const double zA = __shfl_sync(qmask, e, qb + 2 * i1);
+                const double zB = __shfl_sync(qmask, e, qb + 2 * i1 + 1);
+                double sc = 1.0;
+                if (late) {
+                    const double z0 = am == 0 ? 1.0 : zA;
+                    const double z1 = am == 1 ? 1.0 : (am == 0 ? zA : zB);
+                    const double z2 = am == 2 ? 1.0 : zB;
+                    double rest = 0.0;
+                    if (1 < R.na) rest = __dadd_rn(rest, z1);   // reduceat: z0 + sequential (n < 9)
+                    if (2 < R.na) rest = __dadd_rn(rest, z2);
+                    sc = __dadd_rn(z0, rest);
+                    lr = __dadd_rn(cm, __dmul_rn(g, log(sc)));
+                }
+                const double sj = __shfl_sync(qmask, sc, own);
+                if (first) {
+                    // weights z / s: each lane its non-max in-arc of column
+                    // c >> 1, the owner also its column's max (z = 1)
+                    auto arc_of = [&](int k) { return k == 0 ? R.arc[0] : (k == 1 ? R.arc[1] : R.arc[2]); };
+                    if (kk < R.na) C.weights[(size_t)arc_of(kk) * 2 + (c >> 1)] = __ddiv_rn(e, sj);
+                    if (late) C.weights[(size_t)arc_of(am) * 2 + j] = __ddiv_rn(1.0, sc);
+                }
+            }
+        }
+        if (first) {
+            if (HARD) {
+                C.arrival[(size_t)rt * 4 + c] = at;
+                C.slew[(size_t)rt * 4 + c] = sl;
+            }
+            if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = lr;
+        }
+    } else if (kind == ROOT_FEED) {
+        // driven by its parent net's member update (a lower level)
+        at = n_at;
+        sl = n_sl;
+        lr = n_lr;
+    } else {
+        // primary-input root (or undriven): the seeded values
+        at = n_at;
+        sl = n_sl;
+        lr = at;
+        if (first) {
+            if (HARD) {
+                C.arrival[(size_t)rt * 4 + c] = at;
+                C.slew[(size_t)rt * 4 + c] = sl;
+            }
+            if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = at;
+        }
+    }
+}
+
 template <bool HARD, bool LSE, bool STATIC = false>
 __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const Task& T,
                          FwdSmem& S, const FwdRec& R, double g, int plev = -1)
@@ -615,120 +745,8 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
         const int kind = fl & TQ_KIND;
         const int rt = S.n.root[qi];
         double at = 0, sl = 0, lr = 0;
-        if (kind == ROOT_ARC) {
-            if (wide) {
-                fwd_net_wide<HARD, LSE>(t, L, C, S.n.aptr[0], S.n.aptr[1], rt, c, g, first, at, sl, lr);
-            } else if (R.na > FWD_NA) {
-                fwd_net_loop<HARD, LSE>(t, L, C, R.a0, R.a0 + R.na, rt, ld, c, g, first, at, sl, lr);
-            } else {
-                if (HARD) {
-                    // every slot's delay and output slew (independent chains),
-                    // then the ordered merge; the root load is located once
-                    // on the first arc's load axis
-                    const int4 d0 = L.info[R.dl[0]];
-                    const Loc ll0 = lut_locate(L.l + d0.z, d0.w, ld);
-                    double sw[FWD_NA];
-#pragma unroll
-                    for (int k = 0; k < FWD_NA; k++) {
-                        const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
-                        const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
-                        const Loc lld = (di.z == d0.z && di.w == d0.w) ? ll0 : lut_locate(L.l + di.z, di.w, ld);
-                        dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
-                        const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
-                        const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld);
-                        sw[k] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
-                    }
-                    double best = late ? -INF : INF;
-                    sl = sw[0];
-#pragma unroll
-                    for (int k = 0; k < FWD_NA; k++) {
-                        if (k >= R.na) break;
-                        C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
-                        const double v = __dadd_rn(atf[k], dd[k]);
-                        if (later_wins(late, best, v)) { best = v; sl = sw[k]; }
-                    }
-                    at = best;
-                }
-                if (LSE) {
-                    // The LSE of the two late columns, spread over the
-                    // net's 4 lanes: column j's owner (lane 2 + j) forms
-                    // x = lse_at[from] + delay and its first max am; of the
-                    // (column, in-arc) exponentials only the <= 4 non-max
-                    // ones are not exactly 1, so lane c takes column c >> 1's
-                    // (c & 1)-th non-max in-arc: one exp per lane instead
-                    // of three on the late lanes.  Same arithmetic as the
-                    // reference order (np.maximum.reduceat, z0 + sequential
-                    // rest, z / s).
-                    const int qb = threadIdx.x & 28;                 // the quad's cond-0 lane
-                    const unsigned qmask = 0xFu << qb;
-                    double x0 = 0.0, x1 = 0.0, x2 = 0.0, cm = -INF;
-                    int am = 0;
-                    if (late) {
-                        x0 = __dadd_rn(xl[0], dd[0]);
-                        x1 = __dadd_rn(xl[1], dd[1]);
-                        x2 = __dadd_rn(xl[2], dd[2]);
-                        cm = x0;                                       // np.maximum.reduceat
-                        if (1 < R.na && x1 > cm) { cm = x1; am = 1; }
-                        if (2 < R.na && x2 > cm) { cm = x2; am = 2; }
-                    }
-                    const double d0 = __dsub_rn(x0, cm), d1 = __dsub_rn(x1, cm), d2 = __dsub_rn(x2, cm);
-                    const int own = qb + 2 + (c >> 1);                // owner of column c >> 1
-                    const int amj = __shfl_sync(qmask, am, own);
-                    const double dA = __shfl_sync(qmask, am == 0 ? d1 : d0, own);   // first non-max
-                    const double dB = __shfl_sync(qmask, am == 2 ? d1 : d2, own);   // second non-max
-                    const int i1 = c & 1, kk = i1 + (i1 >= amj ? 1 : 0);
-                    const double dm = i1 ? dB : dA;
-                    // the max element's +0 / g = +0 and exp(+0) = 1 need no
-                    // division (whose zero dividend takes the IEEE slow path)
-                    const double e = (kk >= R.na || dm == 0.0) ? 1.0 : exp(__ddiv_rn(dm, g));
-                    const double zA = __shfl_sync(qmask, e, qb + 2 * i1);
-                    const double zB = __shfl_sync(qmask, e, qb + 2 * i1 + 1);
-                    double sc = 1.0;
-                    if (late) {
-                        const double z0 = am == 0 ? 1.0 : zA;
-                        const double z1 = am == 1 ? 1.0 : (am == 0 ? zA : zB);
-                        const double z2 = am == 2 ? 1.0 : zB;
-                        double rest = 0.0;
-                        if (1 < R.na) rest = __dadd_rn(rest, z1);   // reduceat: z0 + sequential (n < 9)
-                        if (2 < R.na) rest = __dadd_rn(rest, z2);
-                        sc = __dadd_rn(z0, rest);
-                        lr = __dadd_rn(cm, __dmul_rn(g, log(sc)));
-                    }
-                    const double sj = __shfl_sync(qmask, sc, own);
-                    if (first) {
-                        // weights z / s: each lane its non-max in-arc of column
-                        // c >> 1, the owner also its column's max (z = 1)
-                        auto arc_of = [&](int k) { return k == 0 ? R.arc[0] : (k == 1 ? R.arc[1] : R.arc[2]); };
-                        if (kk < R.na) C.weights[(size_t)arc_of(kk) * 2 + (c >> 1)] = __ddiv_rn(e, sj);
-                        if (late) C.weights[(size_t)arc_of(am) * 2 + j] = __ddiv_rn(1.0, sc);
-                    }
-                }
-            }
-            if (first) {
-                if (HARD) {
-                    C.arrival[(size_t)rt * 4 + c] = at;
-                    C.slew[(size_t)rt * 4 + c] = sl;
-                }
-                if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = lr;
-            }
-        } else if (kind == ROOT_FEED) {
-            // driven by its parent net's member update (a lower level)
-            at = n_at;
-            sl = n_sl;
-            lr = n_lr;
-        } else {
-            // primary-input root (or undriven): the seeded values
-            at = n_at;
-            sl = n_sl;
-            lr = at;
-            if (first) {
-                if (HARD) {
-                    C.arrival[(size_t)rt * 4 + c] = at;
-                    C.slew[(size_t)rt * 4 + c] = sl;
-                }
-                if (LSE && late) C.lse_at[(size_t)rt * 2 + j] = at;
-            }
-        }
+        fwd_net_item<HARD, LSE>(t, L, C, R, kind, rt, wide, S.n.aptr[0], S.n.aptr[1], first, slf, atf, xl, dd,
+                                ld, n_at, n_sl, n_lr, c, g, at, sl, lr);
         if (HARD) { S.at[qi * 4 + c] = at; S.sl[qi * 4 + c] = sl; }
         if (LSE && late) S.lr[qi * 2 + j] = lr;
     }
