@@ -111,6 +111,7 @@ out = {"round": R, "what": "in-pass time per kernel class of one fused C3 pass (
                           "tail from the ncu launch list; median of 7 passes",
        "pass_us_cuda_events": round(tot_us, 1), "classes_sum_us": round(ssum, 1),
        "classes_over_pass": round(ssum / tot_us, 4), "classes": classes}
-os.makedirs(os.path.join(HERE, "profiles"), exist_ok=True)
-json.dump(out, open(os.path.join(HERE, "profiles", f"inpass_{R}.json"), "w"), indent=1)
+for d in ("profiles", "gpurun_out"):     # gpurun_out/ is what travels back from a GPU box
+    os.makedirs(os.path.join(HERE, d), exist_ok=True)
+    json.dump(out, open(os.path.join(HERE, d, f"inpass_{R}.json"), "w"), indent=1)
 print(json.dumps(out, indent=1))

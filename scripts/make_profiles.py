@@ -11,9 +11,11 @@ import sys
 R = sys.argv[1]
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(HERE, "gpurun_out")
-P = os.path.join(HERE, "profiles")
+# --out DIR: write the summaries there (on a GPU box: under gpurun_out/, the
+# only directory that travels back; the .ncu-rep files are too big to)
+P = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join(HERE, "profiles")
 os.makedirs(P, exist_ok=True)
-for f in (f"bench_{R}.json", f"bench_ref_{R}.json", f"gpu_{R}.txt"):
+for f in (f"bench_{R}.json", f"bench_ref_{R}.json", f"gpu_{R}.txt", f"inpass_{R}.json"):
     if os.path.exists(os.path.join(G, f)):
         shutil.copy(os.path.join(G, f), os.path.join(P, f))
 py = sys.executable
@@ -26,7 +28,7 @@ if os.path.exists(lc):
                  "# per-launch times are cold-cache and serialised: compare shares, not absolutes\n")
         fh.write(out)
     shutil.copy(lc, os.path.join(P, f"launches_{R}.csv"))
-for k in ("fwd", "bwd", "rc", "pglevel", "pgmem", "wire"):
+for k in ("fwd", "bwd", "rc", "pglevel", "pgmem", "wire", "fwd16", "bwd16", "bwdpg"):
     rep = os.path.join(G, f"prof_{k}_{R}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -35,6 +37,10 @@ for k in ("fwd", "bwd", "rc", "pglevel", "pgmem", "wire"):
     with open(os.path.join(P, f"ncu_{k}_{R}.txt"), "w") as fh:
         fh.write(f"# ncu --set full --clock-control none --import-source on (one launch), {os.path.basename(rep)}\n")
         fh.write(s)
+        for tool in ("ncu_stalls.py", "ncu_instr.py"):
+            fh.write(f"\n# scripts/{tool} (top source lines)\n")
+            fh.write(subprocess.run([py, os.path.join(HERE, "scripts", tool), rep, "20"], capture_output=True,
+                                    text=True).stdout)
         fh.write("\n# --page details\n")
         fh.write(d)
 # placement step: the last step's launches (wire + pass + position gradients)

@@ -26,6 +26,14 @@ for topo in ("star", "random_tree"):
     timer.step()
     timer.step(pl.xy + 0.1)
     dev.run(_lib.RUN_WIRE | base | _lib.RUN_POSGRAD, corner=1)
+    # the fused sweep (k_bwd<..., PG>, cp.async prologue) vs the stand-alone one
+    fused = base | _lib.RUN_FUSED | _lib.RUN_WIRE | _lib.RUN_POSGRAD
+    dev.run(fused, corner=0, n_corners=2)
+    a = dev.get("d_xy", 1)
+    os.environ["WS_PG_SWEEP"] = "stream"
+    dev.run(fused, corner=0, n_corners=2)
+    del os.environ["WS_PG_SWEEP"]
+    assert np.array_equal(a, dev.get("d_xy", 1))
     print(topo, dev.summary(), float(np.abs(timer.grad_xy()).max()))
     dev.close()
 d = tempfile.mkdtemp()
