@@ -1019,10 +1019,15 @@ __device__ void pg_task_nets(const Topo& t, const LutView& L, const Corner& C, c
         const int ii = i >> 1, j = i & 1;
         const int fl = S.n.flags[ii], kind = fl & TQ_KIND, root = S.n.root[ii];
         const int mb = S.n.mptr[ii] - T.m0, m = S.n.mptr[ii + 1] - S.n.mptr[ii];
-        double p0 = 0.0, p1 = 0.0;                // member slots 0, 2, 4, ... / 1, 3, 5, ...
-        for (int k = 0; k < m; k += 2) p0 = __dadd_rn(p0, P.pt[(mb + k) * 2 + j]);
-        for (int k = 1; k < m; k += 2) p1 = __dadd_rn(p1, P.pt[(mb + k) * 2 + j]);
-        const double gsum = __dadd_rn(p0, p1);
+        // root-slew terms: 8 interleaved partials P(k mod 8), combined
+        // ((P0 + P1) + (P2 + P3)) + ((P4 + P5) + (P6 + P7)) (pg_net_group's order)
+        double pp[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < m; k += 8)
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+                if (k + a < m) pp[a] = __dadd_rn(pp[a], P.pt[(mb + k + a) * 2 + j]);
+        const double gsum = __dadd_rn(__dadd_rn(__dadd_rn(pp[0], pp[1]), __dadd_rn(pp[2], pp[3])),
+                                      __dadd_rn(__dadd_rn(pp[4], pp[5]), __dadd_rn(pp[6], pp[7])));
         double groot = gsum;
         if (kind == ROOT_FEED) {
             G.gsr[(size_t)root * 2 + j] = gsum;

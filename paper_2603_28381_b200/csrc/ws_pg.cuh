@@ -353,16 +353,21 @@ __device__ void pg_net_group(const Topo& t, const LutView& L, const Corner& C, c
     };
     const Arc arc0 = load_arc(slot);
     wait();
-    // ---- root-slew terms of the members, summed in slot order
-    double part = 0.0;
-#pragma unroll 4
-    for (int r = 0; r < rm; r++) {
-        const int k = r * PS + slot;
-        if (k < m) part = __dadd_rn(part, src.t(f0 + k, mb + k, j));
-    }
-    // fixed-order sum over the slots of column j within the group
-    for (int o = 2; o < GW; o <<= 1) part = __dadd_rn(part, __shfl_xor_sync(WS_FULL, part, o, GW));
-    const double gsum = part;
+    // ---- root-slew terms of the members: the fixed order of
+    // member_term_sum (8 interleaved partials, pairwise combine); slot s of
+    // the group holds the partials of the residues s, s + 2, s + 4, s + 6
+    static_assert(GW == 4, "the root-slew sum order is laid out for 2 slots per column");
+    double x[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < rm; r += 4)
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int k = (r + i) * PS + slot;        // residue k mod 8 = 2 i + slot
+            if (r + i < rm && k < m) x[i] = __dadd_rn(x[i], src.t(f0 + k, mb + k, j));
+        }
+    double y[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) y[i] = __dadd_rn(x[i], __shfl_xor_sync(WS_FULL, x[i], 2, GW));   // P(2i) + P(2i+1)
+    const double gsum = __dadd_rn(__dadd_rn(y[0], y[1]), __dadd_rn(y[2], y[3]));
     // ---- root
     double gl = 0.0, groot = gsum;
     if (act && kind == ROOT_FEED && slot == 0) G.gsr[(size_t)root * 2 + j] = gsum;
