@@ -257,3 +257,24 @@ def test_fused_sweep_equals_stream_sweep(case, monkeypatch):
         dev.close()
     for f, _ in PG_FIELDS:
         assert np.array_equal(out["fused"][f], out["stream"][f], equal_nan=True), f
+
+
+@pytest.mark.parametrize("nc", [5, 16])
+def test_place_candidate_batch_bitwise_single(nc):
+    """A batch of nc placement candidates in one ws_run (k_wire, the pass and
+    the fused sweep with blockIdx.y = candidate; the 4-block level-kernel
+    variants for nc >= 4 outside the sweep) equals nc single-candidate runs
+    bit for bit, chunked big star nets and wide nets included; candidate 0
+    also matches the oracle."""
+    raw = _sweep_case("big_star")
+    pls = [PL.synthetic_placement(raw, seed=20 + k) for k in range(nc)]
+    dev = ws.DeviceDesign(raw, n_corners=nc)
+    timers = [PL.PlacementTimer(dev, pls[k], corner=k, graph=False) for k in range(nc)]
+    dev.run(PL.PlacementTimer.FLAGS, corner=0, n_corners=nc)
+    batch = [{f: dev.get(f, k) for f, _ in PG_FIELDS} for k in range(nc)]
+    check(dev, 0, raw, pls[0])
+    for k in range(nc):
+        timers[k].step()
+        for f, _ in PG_FIELDS:
+            assert np.array_equal(dev.get(f, k), batch[k][f], equal_nan=True), (k, f)
+    dev.close()
