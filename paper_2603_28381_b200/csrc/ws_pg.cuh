@@ -20,6 +20,25 @@ namespace pg {
 
 constexpr double PG_INF = __builtin_huge_val();
 
+// the located cell of a query on an n > 1 point axis: upper_bound - 1
+// clamped to [0, n - 2] (_kernels.pyx:15-81), by lut_locate's branch-free
+// halving steps for n <= 8
+__device__ __forceinline__ int axis_cell(const double* ax, int n, double q)
+{
+    int lo;
+    if (n <= 8) {
+        lo = 0;
+#pragma unroll
+        for (int s = 8; s >= 1; s >>= 1)
+            if (lo + s <= n && ax[lo + s - 1] <= q) lo += s;
+    } else {
+        lo = upper_bound_long(ax, n, q);
+    }
+    int i = lo - 1;
+    if (i < 0) i = 0; else if (i > n - 2) i = n - 2;
+    return i;
+}
+
 // d out / d qs and d out / d ql of _interp (_kernels.pyx:15-81) inside the
 // located cell; 0 along an axis whose fraction was clamped (orc interp_grad)
 __device__ __forceinline__ void interp_grad(const LutView& L, int lut, double qs, double ql, double& ds,
@@ -32,26 +51,14 @@ __device__ __forceinline__ void interp_grad(const LutView& L, int lut, double qs
     double st, lt, hs = 0.0, hl = 0.0;
     bool fs = false, fl = false;
     if (nS > 1) {
-        int lo = 0, hi = nS;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (L.s[s0 + mid] <= qs) lo = mid + 1; else hi = mid;
-        }
-        si = lo - 1;
-        if (si < 0) si = 0; else if (si > nS - 2) si = nS - 2;
+        si = axis_cell(L.s + s0, nS, qs);
         hs = __dsub_rn(L.s[s0 + si + 1], L.s[s0 + si]);
         st = __ddiv_rn(__dsub_rn(qs, L.s[s0 + si]), hs);
         if (st < 0.0) st = 0.0; else if (st > 1.0) st = 1.0; else fs = true;
         si2 = si + 1;
     } else { si = 0; st = 0.0; si2 = 0; }
     if (nL > 1) {
-        int lo = 0, hi = nL;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (L.l[l0 + mid] <= ql) lo = mid + 1; else hi = mid;
-        }
-        li = lo - 1;
-        if (li < 0) li = 0; else if (li > nL - 2) li = nL - 2;
+        li = axis_cell(L.l + l0, nL, ql);
         hl = __dsub_rn(L.l[l0 + li + 1], L.l[l0 + li]);
         lt = __ddiv_rn(__dsub_rn(ql, L.l[l0 + li]), hl);
         if (lt < 0.0) lt = 0.0; else if (lt > 1.0) lt = 1.0; else fl = true;
