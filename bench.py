@@ -777,6 +777,7 @@ def main():
     t_gen = time.time() - t0
     t0 = time.time()
     dev = ws.DeviceDesign(raw, n_corners=2)     # two slots: pass i runs slot i % 2
+    dev_levels = dev.n_levels
     torch.cuda.synchronize()
     t_build = time.time() - t0
     if world > 1 or rank > 0:
@@ -969,8 +970,24 @@ def main():
                 "clocks": clk.summary(),
                 "result": {"tns": tns, "wns": wns, "loss": loss},
                 "init": {"generate_s": round(t_gen, 2), "device_build_ms": round(t_build * 1e3, 1)}}
-        if "classes" in prof:
-            line["roofline"]["kernel_classes"] = prof["classes"].get("classes")
+        if "classes" in prof and args.workload == "c3":     # the profiles are C3's
+            cls = [dict(c) for c in prof["classes"].get("classes", [])]
+            # per-class achieved GB/s on SURVEY §8(d)'s compulsory bytes: the
+            # RC kernel's own (res / cap 64 B per member, root_cap 32 B per
+            # net, load / delay / impulse 96 B per pin), the tail's (36 B per
+            # endpoint), the rest spread over the 2L level launches
+            b_rc = 64 * raw.n_members + 32 * raw.n_nets + 96 * raw.n_pins
+            b_tail = 36 * len(raw.ep_pin)
+            b_lvl = (B - b_rc - b_tail) / max(1, 2 * dev_levels)
+            for c in cls:
+                k, n = c.get("kernel", ""), max(1, c.get("launches_per_pass", 1))
+                byt = b_rc if k.startswith("k_rc") else (b_tail if "summary" in k else b_lvl * n)
+                us = c.get("in_pass_us")
+                if us:
+                    c["algorithmic_bytes"] = int(byt)
+                    c["achieved_gbs"] = round(byt / (us * 1e-6) / 1e9, 1)
+                    c["frac"] = round(byt / (us * 1e-6) / 1e9 / peak, 4)
+            line["roofline"]["kernel_classes"] = cls
             line["roofline"]["kernel_classes_source"] = prof["classes"].get("what")
         if "traffic" in prof:
             line["roofline"]["traffic_source"] = prof["traffic"].get("what")
