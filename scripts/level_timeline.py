@@ -41,9 +41,15 @@ for i in range(1, 2 * L + 1):
         late = int((st > prev_end).sum())
         lag = (rel.min() - prev_end) / 1e3
         j = int(np.argmax(end))
+        early = st < prev_end - 5000        # started > 5 us before the previous level's end
+        lateb = st > prev_end - 2000        # started in its last 2 us
         rows.append(("fwd" if i <= L else "bwd", len(b), late, lag, (st[j] - prev_end) / 1e3,
                      (rec[j] - st[j]) / 1e3, (rel[j] - max(rec[j], prev_end)) / 1e3, (end[j] - rel[j]) / 1e3,
-                     (end.max() - prev_end) / 1e3, np.median(end - rel) / 1e3))
+                     (end.max() - prev_end) / 1e3, np.median(end - rel) / 1e3,
+                     np.median((rec - st)[early]) / 1e3 if early.any() else np.nan,
+                     np.median((rec - st)[lateb]) / 1e3 if lateb.any() else np.nan,
+                     int(early.sum()), int(lateb.sum()),
+                     np.median((st - prev_end) / 1e3)))
     prev_end = end.max()
 for kind in ("fwd", "bwd"):
     R = np.array([r[1:] for r in rows if r[0] == kind], dtype=np.float64)
@@ -51,3 +57,6 @@ for kind in ("fwd", "bwd"):
     print(f"{kind}: blocks {m[0]:.0f}, started after the previous level's end {m[1]:.0f}, "
           f"PDL release lag {m[2]:.2f} us | last-finishing block: start {m[3]:+.2f}, records {m[4]:.2f}, "
           f"wait after records {m[5]:.2f}, body {m[6]:.2f} | level step {m[7]:.2f} us, median body {m[8]:.2f}")
+    m2 = np.nanmedian(R[:, 9:], axis=0)
+    print(f"   records phase: blocks started >5 us before the previous end {m2[2]:.0f} (median {m2[0]:.2f} us), "
+          f"in its last 2 us {m2[3]:.0f} (median {m2[1]:.2f} us); median start {m2[4]:+.2f} us")
