@@ -391,12 +391,13 @@ def corner_batch(raw, rank, world, steps, flush, dist=None, n_total=16):
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush.fill_(0)
-    e0.record(stream)
-    for i in range(steps):
-        step(i)
-    stream.wait_stream(side)                       # the last exchange is inside the region
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for i in range(steps):
+            step(i)
+        stream.wait_stream(side)                       # the last exchange is inside the region
+        e1.record(stream)
+        torch.cuda.synchronize()
     tot = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -405,7 +406,7 @@ def corner_batch(raw, rank, world, steps, flush, dist=None, n_total=16):
     out = {"workload": "C5: %d corners of the C3 netlist, corner k -> rank k mod N, a rank's corners "
                        "in one ws_run with the in-kernel batch gradient sum, then NCCL TNS/loss SUM, "
                        "WNS MIN, gradient SUM on a side stream overlapped with the next batch" % n_total,
-           "corners_per_gpu": nc, "ms_per_batch": round(ms, 4),
+           "corners_per_gpu": nc, "ms_per_batch": round(ms, 4), "clocks": clk.summary(),
            "corners_per_s": round(n_total / (ms * 1e-3), 2), "steps": steps,
            "gpu_launches_per_batch": launches,
            "achieved_gbs": round(n_total * C3_BYTES / (ms * 1e-3) / 1e9, 1),
@@ -453,11 +454,12 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
     if dist is not None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(steps):
-        s, _ = step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for i in range(steps):
+            s, _ = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
     tot = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -466,7 +468,7 @@ def candidate_batch(raw, rank, world, steps, dist=None, n_total=16, sigma_um=0.5
     out = {"workload": "%d placement candidates of C3 (cells moved by N(0, %.1f um)), candidate c -> "
                        "rank c mod N, a rank's candidates in one ws_run with position gradients, "
                        "(TNS, WNS, loss) and dL/dxy all-gathered" % (n_total, sigma_um),
-           "candidates_per_gpu": nc, "ms_per_batch": round(ms, 4),
+           "candidates_per_gpu": nc, "ms_per_batch": round(ms, 4), "clocks": clk.summary(),
            "candidates_per_s": round(n_total / (ms * 1e-3), 2), "steps": steps,
            "best": {"candidate": b, "loss": float(s[b, 2]), "tns": float(s[b, 0])}}
     dev.close()
@@ -932,7 +934,7 @@ def main():
     cb = pb = None
     if args.corners and 16 % world == 0:
         cb = corner_batch(raw, rank, world, steps=max(3, min(args.steps, 10)), flush=flush, dist=dist)
-        pb = candidate_batch(raw, rank, world, steps=6, dist=dist)
+        pb = candidate_batch(raw, rank, world, steps=12, dist=dist)
 
     if rank == 0:
         P, M, N, A, I, E = (raw.n_pins, raw.n_members, raw.n_nets, raw.n_arcs, len(raw.pi_pin),
