@@ -247,10 +247,12 @@ __device__ __forceinline__ Loc lut_locate(const double* ax, int n, double q)
         int lo;
         if (n <= 8) {
             // upper_bound on a sorted axis = number of entries <= q (a
-            // monotone prefix): four fixed branch-free halving steps
+            // monotone prefix): three fixed branch-free halving steps reach
+            // lo <= 7; for n = 8, lo = 7 and lo = 8 clamp to the same cell
+            // (n - 2), so the fourth step of a full search is not needed
             lo = 0;
 #pragma unroll
-            for (int s = 8; s >= 1; s >>= 1)
+            for (int s = 4; s >= 1; s >>= 1)
                 if (lo + s <= n && ax[lo + s - 1] <= q) lo += s;
         } else {
             lo = upper_bound_long(ax, n, q);

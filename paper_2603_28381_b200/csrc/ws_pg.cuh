@@ -21,15 +21,15 @@ namespace pg {
 constexpr double PG_INF = __builtin_huge_val();
 
 // the located cell of a query on an n > 1 point axis: upper_bound - 1
-// clamped to [0, n - 2] (_kernels.pyx:15-81), by lut_locate's branch-free
-// halving steps for n <= 8
+// clamped to [0, n - 2] (_kernels.pyx:15-81), by lut_locate's three
+// branch-free halving steps for n <= 8
 __device__ __forceinline__ int axis_cell(const double* ax, int n, double q)
 {
     int lo;
     if (n <= 8) {
         lo = 0;
 #pragma unroll
-        for (int s = 8; s >= 1; s >>= 1)
+        for (int s = 4; s >= 1; s >>= 1)
             if (lo + s <= n && ax[lo + s - 1] <= q) lo += s;
     } else {
         lo = upper_bound_long(ax, n, q);
