@@ -1289,8 +1289,16 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
                     if (later_wins(mx, rr, v)) rr = v;
                 }
             } else {
-                for (int k = k0m; k < k1m; k++)
-                    if (later_wins(mx, rr, S.v[k * 4 + c])) rr = S.v[k * 4 + c];
+                // the ordered max / min fold as one max over sign-flipped
+                // values (the flips are exact: ties, signed zeros and NaN
+                // stickiness are those of later_wins)
+                const double sg = mx ? 1.0 : -1.0;
+                double rs = __dmul_rn(sg, rr);
+                for (int k = k0m; k < k1m; k++) {
+                    const double v = __dmul_rn(sg, S.v[k * 4 + c]);
+                    if (v > rs) rs = v;
+                }
+                rr = __dmul_rn(sg, rs);
             }
             C.required[(size_t)rt * 4 + c] = rr;
             if (!(fq & TQ_ROOT_MEMBER))
