@@ -1279,6 +1279,10 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
     if (ii < T.nq) {
         const int rt = S.n.root[ii], fq = S.n.flags[ii];
         const int k0m = S.n.mptr[ii] - T.m0, k1m = S.n.mptr[ii + 1] - T.m0;
+        // star / small-tree nets of ordinary tasks: one reverse pass over the
+        // members does the required fold and (late columns) the adjoint sum
+        const bool fold_sum = HARD && GRAD && late && !loop && !(fq & TQ_TREE);
+        double ar = n_seed;
         if (HARD) {
             const bool mx = c < 2;
             double rr = n_rr;
@@ -1290,23 +1294,28 @@ __device__ void bwd_body(const Topo& t, const Corner& C, const Task& T, BwdSmem&
                 }
             } else {
                 // the ordered max / min fold as one max over sign-flipped
-                // values (the flips are exact: ties, signed zeros and NaN
-                // stickiness are those of later_wins)
+                // values (the flips are exact), members visited deepest
+                // first with ties to the earlier member (>=), the root's
+                // initial value ahead of them all (>): ties, signed zeros
+                // and NaN stickiness are those of the forward later_wins fold
                 const double sg = mx ? 1.0 : -1.0;
-                double rs = __dmul_rn(sg, rr);
-                for (int k = k0m; k < k1m; k++) {
+                double ms = -INF;
+                for (int k = k1m - 1; k >= k0m; k--) {
                     const double v = __dmul_rn(sg, S.v[k * 4 + c]);
-                    if (v > rs) rs = v;
+                    if (v >= ms) ms = v;
+                    if (fold_sum) ar = __dadd_rn(ar, S.de[k * 2 + j]);
                 }
-                rr = __dmul_rn(sg, rs);
+                const double rs0 = __dmul_rn(sg, rr);
+                rr = __dmul_rn(sg, ms > rs0 ? ms : rs0);
             }
             C.required[(size_t)rt * 4 + c] = rr;
             if (!(fq & TQ_ROOT_MEMBER))
                 C.slack[(size_t)rt * 4 + c] = mx ? __dsub_rn(n_at, rr) : __dsub_rn(rr, n_at);
         }
         if (GRAD && late) {
-            double ar = n_seed;
-            if ((fq & TQ_TREE) || loop) {
+            if (fold_sum) {
+                // summed with the fold above
+            } else if ((fq & TQ_TREE) || loop) {
                 // parents gather children, deepest member first (diff.py:222-233)
                 const int s = S.n.f0[ii];
                 for (int k = k1m - k0m - 1; k >= 0; k--) {
