@@ -963,8 +963,9 @@ __device__ __forceinline__ void bwd_gather(const Corner& C, int pin, int fl, int
     if (HARD) {
         if (fl & TM_ROOT) r0 = LDG(C.required + (size_t)pin * 4 + c);
         else if (fl & TM_MULTI_EP) r0 = init_required_multi(t, C, pin, c);
-        else r0 = merge_req(c < 2 ? -INF : INF, (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c]
-                                                            : (c < 2 ? -INF : INF), c);
+        // merge_req(+-INF, x) is x bit for bit (x = +-INF returns the same
+        // infinity, NaN stays NaN): the single endpoint RAT or the identity
+        else r0 = (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c] : (c < 2 ? -INF : INF);
         if (o1a >= 0) {
             rto = LDG(C.required + (size_t)o1t * 4 + c);
             ado = LDG(C.arc_delay + (size_t)o1a * 4 + c);
@@ -986,8 +987,8 @@ __device__ __forceinline__ double root_init_required(const Topo& t, const Corner
                                                       int e1, int c)
 {
     if (fq & TQ_MULTI_EP) return init_required_multi(t, C, rt, c);
-    return merge_req(c < 2 ? -INF : INF,
-                     (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)e1 * 4 + c] : (c < 2 ? -INF : INF), c);
+    // merge_req(+-INF, x) == x bit for bit
+    return (fq & TQ_ROOT_EP) ? C.ep_required[(size_t)e1 * 4 + c] : (c < 2 ? -INF : INF);
 }
 
 __device__ __forceinline__ double root_seed(const Topo& t, const Corner& C, int rt, int fq, int e1,
