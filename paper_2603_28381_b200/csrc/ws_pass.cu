@@ -923,7 +923,9 @@ __device__ __forceinline__ void bwd_member(const Topo& t, const Corner& C, int o
 {
     if (HARD) {
         const bool mx = c < 2;
-        double r = r0;
+        // pins with several endpoint entries merge their RATs here, not in
+        // the gather round (keeps its loads straight-line)
+        double r = ((fl & TM_MULTI_EP) && !(fl & TM_ROOT)) ? init_required_multi(t, C, pin, c) : r0;
         if (o1 > o0) {
             const double vv = __dsub_rn(rto, ado);
             if (later_wins(mx, r, vv)) r = vv;
@@ -962,7 +964,7 @@ __device__ __forceinline__ void bwd_gather(const Corner& C, int pin, int fl, int
     const int j = c - 2;
     if (HARD) {
         if (fl & TM_ROOT) r0 = LDG(C.required + (size_t)pin * 4 + c);
-        else if (fl & TM_MULTI_EP) r0 = init_required_multi(t, C, pin, c);
+        else if (fl & TM_MULTI_EP) r0 = 0.0;      // merged in bwd_member
         // merge_req(+-INF, x) is x bit for bit (x = +-INF returns the same
         // infinity, NaN stays NaN): the single endpoint RAT or the identity
         else r0 = (fl & TM_EP) ? C.ep_required[(size_t)e1 * 4 + c] : (c < 2 ? -INF : INF);
