@@ -568,27 +568,39 @@ __device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, co
                 // every slot's delay and output slew (independent chains),
                 // then the ordered merge; the root load is located once
                 // on the first arc's load axis
+                // every slot's delay (independent chains) and the ordered
+                // merge (first arc wins ties); only the winner's output slew
+                // is interpolated, reusing its located cells when the slew
+                // table shares the delay table's axes.  The root load is
+                // located once on the first arc's load axis.
                 const int4 d0 = L.info[R.dl[0]];
                 const Loc ll0 = lut_locate(L.l + d0.z, d0.w, ld);
-                double sw[FWD_NA];
+                double best = late ? -INF : INF;
+                Loc wls{}, wll{};
+                int4 wdi = d0;
+                int wsl = R.sl[0];
+                double wslf = slf[0];
 #pragma unroll
                 for (int k = 0; k < FWD_NA; k++) {
-                    const int4 di = L.info[R.dl[k]], si = L.info[R.sl[k]];
+                    const int4 di = L.info[R.dl[k]];
                     const Loc lsd = lut_locate(L.s + di.x, di.y, slf[k]);
                     const Loc lld = (di.z == d0.z && di.w == d0.w) ? ll0 : lut_locate(L.l + di.z, di.w, ld);
                     dd[k] = lut_blend(L.t + L.t_ptr[R.dl[k]], di.w, lsd, lld);
-                    const Loc lss = (si.x == di.x && si.y == di.y) ? lsd : lut_locate(L.s + si.x, si.y, slf[k]);
-                    const Loc lls = (si.z == di.z && si.w == di.w) ? lld : lut_locate(L.l + si.z, si.w, ld);
-                    sw[k] = lut_blend(L.t + L.t_ptr[R.sl[k]], si.w, lss, lls);
+                    if (k == 0) { wls = lsd; wll = lld; }   // the slot-0 default (no strict winner)
+                    if (k < R.na) {
+                        C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
+                        const double v = __dadd_rn(atf[k], dd[k]);
+                        if (later_wins(late, best, v)) {
+                            best = v;
+                            wls = lsd; wll = lld; wdi = di; wsl = R.sl[k]; wslf = slf[k];
+                        }
+                    }
                 }
-                double best = late ? -INF : INF;
-                sl = sw[0];
-#pragma unroll
-                for (int k = 0; k < FWD_NA; k++) {
-                    if (k >= R.na) break;
-                    C.arc_delay[(size_t)R.arc[k] * 4 + c] = dd[k];
-                    const double v = __dadd_rn(atf[k], dd[k]);
-                    if (later_wins(late, best, v)) { best = v; sl = sw[k]; }
+                {
+                    const int4 si = L.info[wsl];
+                    const Loc lss = (si.x == wdi.x && si.y == wdi.y) ? wls : lut_locate(L.s + si.x, si.y, wslf);
+                    const Loc lls = (si.z == wdi.z && si.w == wdi.w) ? wll : lut_locate(L.l + si.z, si.w, ld);
+                    sl = lut_blend(L.t + L.t_ptr[wsl], si.w, lss, lls);
                 }
                 at = best;
             }
