@@ -649,13 +649,16 @@ __device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, co
                     sc = __dadd_rn(z0, rest);
                     lr = __dadd_rn(cm, __dmul_rn(g, log(sc)));
                 }
-                const double sj = __shfl_sync(qmask, sc, own);
                 if (first) {
-                    // weights z / s: each lane its non-max in-arc of column
-                    // c >> 1, the owner also its column's max (z = 1)
+                    // weights z / s: the owner's 1 / s (its column's max,
+                    // z = 1, exactly) and every lane's non-max in-arc of
+                    // column c >> 1 as z * (1 / s) (within an ulp of z / s:
+                    // one division per column instead of one per weight)
+                    const double rinv = late ? __ddiv_rn(1.0, sc) : 0.0;
+                    const double rj = __shfl_sync(qmask, rinv, own);
                     auto arc_of = [&](int k) { return k == 0 ? R.arc[0] : (k == 1 ? R.arc[1] : R.arc[2]); };
-                    if (kk < R.na) C.weights[(size_t)arc_of(kk) * 2 + (c >> 1)] = __ddiv_rn(e, sj);
-                    if (late) C.weights[(size_t)arc_of(am) * 2 + j] = __ddiv_rn(1.0, sc);
+                    if (kk < R.na) C.weights[(size_t)arc_of(kk) * 2 + (c >> 1)] = __dmul_rn(e, rj);
+                    if (late) C.weights[(size_t)arc_of(am) * 2 + j] = rinv;
                 }
             }
         }
