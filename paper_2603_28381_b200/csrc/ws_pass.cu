@@ -554,7 +554,7 @@ __device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, co
                                              int kind, int rt, bool wide, int wa0, int wa1, bool first,
                                              const double* slf, const double* atf, const double* xl, double* dd,
                                              double ld, double n_at, double n_sl, double n_lr, int c, double g,
-                                             double& at, double& sl, double& lr)
+                                             double ginv, double& at, double& sl, double& lr)
 {
     const bool late = c >= 2;
     const int j = c - 2;
@@ -635,7 +635,9 @@ __device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, co
                 const double dm = i1 ? dB : dA;
                 // the max element's +0 / g = +0 and exp(+0) = 1 need no
                 // division (whose zero dividend takes the IEEE slow path)
-                const double e = (kk >= R.na || dm == 0.0) ? 1.0 : exp(__ddiv_rn(dm, g));
+                // exp((x - max) / gamma) with 1 / gamma from the host (the
+                // argument within an ulp and a half of the quotient's)
+                const double e = (kk >= R.na || dm == 0.0) ? 1.0 : exp(__dmul_rn(dm, ginv));
                 const double zA = __shfl_sync(qmask, e, qb + 2 * i1);
                 const double zB = __shfl_sync(qmask, e, qb + 2 * i1 + 1);
                 double sc = 1.0;
@@ -691,7 +693,7 @@ __device__ __forceinline__ void fwd_net_item(const Topo& t, const LutView& L, co
 
 template <bool HARD, bool LSE, bool STATIC = false>
 __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const Task& T,
-                         FwdSmem& S, const FwdRec& R, double g, int plev = -1)
+                         FwdSmem& S, const FwdRec& R, double g, double ginv, int plev = -1)
 {
     const int tid = threadIdx.x, c = tid & 3, qi = tid >> 2;
     const bool late = c >= 2;
@@ -761,7 +763,7 @@ __device__ void fwd_body(const Topo& t, const LutView& L, const Corner& C, const
         const int rt = S.n.root[qi];
         double at = 0, sl = 0, lr = 0;
         fwd_net_item<HARD, LSE>(t, L, C, R, kind, rt, wide, S.n.aptr[0], S.n.aptr[1], first, slf, atf, xl, dd,
-                                ld, n_at, n_sl, n_lr, c, g, at, sl, lr);
+                                ld, n_at, n_sl, n_lr, c, g, ginv, at, sl, lr);
         if (HARD) { S.at[qi * 4 + c] = at; S.sl[qi * 4 + c] = sl; }
         if (LSE && late) S.lr[qi * 2 + j] = lr;
     }
@@ -1619,7 +1621,7 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_rc(Topo t, Corners cs, int w, i
 // throughput-bound and run a 4-block variant (WS_MINB_BATCH).
 template <bool HARD, bool LSE, int MB = WS_MINB>
 __global__ void __launch_bounds__(PASS_TPB, MB) k_fwd(Topo t, LutSrc ls, Corners cs, int k0,
-                                                     bool use_smem, double g)
+                                                     bool use_smem, double g, double ginv)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ FwdSmem S;
@@ -1635,7 +1637,7 @@ __global__ void __launch_bounds__(PASS_TPB, MB) k_fwd(Topo t, LutSrc ls, Corners
     LSTAMP(1);
     pdl_wait();          // the previous level's results are now visible
     LSTAMP(2);
-    fwd_body<HARD, LSE>(t, L, C, T, S, R, g);
+    fwd_body<HARD, LSE>(t, L, C, T, S, R, g, ginv);
     LSTAMP(3);
 }
 
@@ -2376,6 +2378,7 @@ template <bool LSE, bool GRAD>
 __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners cs, SumArgs P,
                                                       int w, double g, int kind, bool use_smem)
 {
+    const double ginv = __ddiv_rn(1.0, g);      // = the host's 1.0 / g (correctly rounded)
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PassSmem S;
     __shared__ BlobBuf blob[2];
@@ -2440,7 +2443,7 @@ __global__ void __launch_bounds__(PASS_TPB, 2) k_pass(Topo t, LutSrc ls, Corners
             while (cur.k >= 0 && cur.step == li) {
                 if (!have) { take(false, R, RB_unused); fetch_next(); }
                 fwd_stage_take<true>(stg.f, R);
-                fwd_body<true, LSE, true>(t, L, C, T, S.f, R, g, li);
+                fwd_body<true, LSE, true>(t, L, C, T, S.f, R, g, ginv, li);
                 buf ^= 1;
                 cur = nxt;
                 have = false;
@@ -2683,10 +2686,10 @@ struct Launcher {
         if (nt <= 0) return;
         if (H && Lse && nc >= 4)
             launch(k_fwd<H, Lse, WS_MINB_BATCH>, dim3(nt, nc), dim3(PASS_TPB), lut_bytes, s, probed(nt), ls,
-                   cs, ctx.lvt_ptr_host[li], use_smem, g);
+                   cs, ctx.lvt_ptr_host[li], use_smem, g, 1.0 / g);
         else
             launch(k_fwd<H, Lse>, dim3(nt, nc), dim3(PASS_TPB), H ? lut_bytes : 0, s, probed(nt), ls, cs,
-                   ctx.lvt_ptr_host[li], use_smem, g);
+                   ctx.lvt_ptr_host[li], use_smem, g, 1.0 / g);
         count++;
     }
     template <bool H, bool G>
