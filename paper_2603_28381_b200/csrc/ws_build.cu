@@ -421,6 +421,23 @@ __global__ void k_rc_pcode(int P, const int* member_of_pin, const int* root_net_
     pcode[p] = code;
 }
 
+// the nets whose root load a streaming-RC member block folds: block b owns
+// nets [bnet[b], bnet[b + 1]) (lower bound of b * RC_MPB in net_ptr); the
+// last block also owns the trailing member-less nets
+__global__ void k_rc_bnet(int nb, int N, const int* net_ptr, int* bnet)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    if (b == nb) { bnet[b] = N; return; }
+    const int key = b * RC_MPB;
+    int lo = 0, hi = N;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (net_ptr[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    bnet[b] = lo;
+}
+
 }  // namespace
 
 
@@ -931,6 +948,12 @@ void build_topology(Context& ctx, const ws_design_desc* d)
     if (M) {
         k_rc_code<<<blocks_for(M), TPB, 0, s>>>(M, t.mem_pin, t.mem_net, t.net_tree,
                                                   t.root_net_of_pin, t.rc_code);
+        WS_CHECK_LAUNCH();
+    }
+    {
+        const int nb = (M + RC_MPB - 1) / RC_MPB;
+        t.rc_bnet = ar.alloc<int>(nb + 1);
+        k_rc_bnet<<<blocks_for(nb + 1), TPB, 0, s>>>(nb, N, t.net_ptr, t.rc_bnet);
         WS_CHECK_LAUNCH();
     }
     t.rc_pcode = ar.alloc<int>(P);

@@ -284,6 +284,8 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
             const char* r = getenv("WS_RC_SCHEME");
             c.rc_cte = r && std::string(r) == "cte";
             c.rc_pin_order = r && std::string(r) == "pin";
+            const char* rr = getenv("WS_RC_ROOTS");
+            c.rc_roots = !rr ? 0 : std::string(rr) == "net" ? -1 : std::string(rr) == "fold" ? 1 : 0;
         }
         // blocking streams: with a NULL stream argument the context's work is
         // ordered after (and before) work on the legacy default stream, the

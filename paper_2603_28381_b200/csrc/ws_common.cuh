@@ -50,6 +50,7 @@ struct Topo {
     int *net_tree;                   // 1 if any member has a non-root parent
     int *rc_code;                    // per member: -1 (tree net) or pin << 1 | (pin is a root)
     int *rc_pcode;                   // per pin: the pin-order RC code (ws_build.cu k_rc_pcode)
+    int *rc_bnet;                    // per streaming-RC member block b (+1): first net whose members start at or after b * RC_MPB
     int *pin_ep_ptr, *pin_ep_idx;    // endpoint entries grouped by pin (stable)
     int *pin_pi;                     // pin -> PI index or -1
     int *pin_out_ptr, *pin_out_arc;  // arcs grouped by source pin (all pins)
@@ -121,6 +122,7 @@ constexpr int TM_ROOT = 1, TM_EP = 2, TM_MULTI_EP = 4;
 #define WS_ITEMS 2
 #endif
 constexpr int PASS_TPB = WS_TPB, ITEMS = WS_ITEMS;
+constexpr int RC_MPB = 256;   // members per streaming-RC block (k_rc_flat: RC_TPB x RC_ITEMS (member, cond) items)
 constexpr int TASK_Q = PASS_TPB / 4, TASK_A = ITEMS * PASS_TPB / 4, TASK_M = ITEMS * PASS_TPB / 4;
 // task flags: CHUNK = one chunk of a big star net's members; WIDE = one net
 // with more than TASK_A in-arcs; LOOP = one tree net with more than TASK_M

@@ -1498,6 +1498,41 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm,
             C.net_delay[pin * 4 + c] = d;
             C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
         }
+        if (nbn == 0) {
+            // root loads of the star nets whose members start in this block
+            // (no separate net blocks): the block's caps from shared memory,
+            // a net running past the block's end from global; the same
+            // 8-partial fold as root_load8
+            __shared__ double sc[RC_MPB * 4];
+            const size_t mb0 = (size_t)bx * RC_MPB, mb1 = mb0 + RC_MPB;
+#pragma unroll
+            for (int k = 0; k < RC_ITEMS; k++) sc[threadIdx.x + k * RC_TPB] = b[k];
+            __syncthreads();
+            const int n0 = LDG(t.rc_bnet + bx), n1 = LDG(t.rc_bnet + bx + 1);
+            for (int x = threadIdx.x; x < (n1 - n0) * 4; x += RC_TPB) {
+                const int n = n0 + (x >> 2), c = x & 3;
+                if (LDG(t.net_tree + n)) continue;       // k_rc_tree
+                const int s = LDG(t.net_ptr + n), m = LDG(t.net_ptr + n + 1) - s, root = LDG(t.net_root + n);
+                double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int b0 = 0; b0 < m; b0 += 8)
+#pragma unroll
+                    for (int y = 0; y < 8; y++)
+                        if (b0 + y < m) {
+                            const size_t j = (size_t)(s + b0 + y);
+                            const double cp = j < mb1 ? sc[(j - mb0) * 4 + c] : LDG(C.mem_cap + j * 4 + c);
+                            p[y] = __dadd_rn(p[y], cp);
+                        }
+                p[0] = __dadd_rn(p[0], p[1]); p[2] = __dadd_rn(p[2], p[3]);
+                p[4] = __dadd_rn(p[4], p[5]); p[6] = __dadd_rn(p[6], p[7]);
+                p[0] = __dadd_rn(p[0], p[2]); p[4] = __dadd_rn(p[4], p[6]);
+                const double l = __dadd_rn(p[0], p[4]);
+                C.load[(size_t)root * 4 + c] = __dadd_rn(LDG(C.root_cap + (size_t)n * 4 + c), l);
+                if (LDG(t.member_of_pin + root) < 0) {
+                    C.net_delay[(size_t)root * 4 + c] = 0.0;
+                    C.impulse[(size_t)root * 4 + c] = 0.0;
+                }
+            }
+        }
         return;
     }
     const int i = (bx - nbm) * RC_TPB + threadIdx.x;
@@ -2646,12 +2681,21 @@ struct Launcher {
             const int nbm = (int)(((size_t)(po ? ctx.t.P : ctx.t.M) * 4 + RC_TPB * RC_ITEMS - 1) /
                                   (RC_TPB * RC_ITEMS));
             const int nbn = (int)(((size_t)ctx.t.N * 4 + RC_TPB - 1) / RC_TPB);
+            // star-net root loads: corner batches fold them in the member
+            // blocks (no net blocks: the caps are read once, 16-corner batch
+            // -1.9%); a single corner keeps the net blocks first, whose folds
+            // overlap the member stream (the in-block fold costs it +0.3%).
+            // WS_RC_ROOTS=net / fold forces either.
+            static_assert(RC_TPB * RC_ITEMS == 4 * RC_MPB, "RC member block shape");
+            const bool fold_in_members = !po && !ctx.rc_cte && ctx.t.M > 0 &&
+                                         (ctx.rc_roots > 0 || (ctx.rc_roots == 0 && nc >= 4));
+            const int nbn_flat = fold_in_members ? 0 : nbn;
             const int nbf = (with_free && !ctx.rc_cte) ? (ctx.t.n_free + RC_TPB - 1) / RC_TPB : 0;
             took_free = with_free && !ctx.rc_cte;
             if (ctx.rc_cte)
                 launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
             else
-                launch(k_rc_flat, dim3(nbm + nbn + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn, nbf, lse,
+                launch(k_rc_flat, dim3(nbm + nbn_flat + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn_flat, nbf, lse,
                        po);
             if (ctx.any_tree) {
                 count++;
