@@ -150,6 +150,7 @@ struct Context {
     SumPlan* tns_plan = nullptr;      // over 2E slack terms
     int launches_last_run = 0;
     bool lut_global = false;
+    int split_min = 8;           // WS_SPLIT=n: fused corner batches of >= n corners run as two half batches on two streams (0: never)
     int rc_roots = 0;            // WS_RC_ROOTS: star-net root loads in net blocks (net, -1) / member blocks (fold, 1) / by batch size (0)
     bool rc_pin_order = false;   // WS_RC_SCHEME=pin: the pin-order streaming RC
     bool rc_cte = false;       // WS_RC_SCHEME=cte: the paper's CTE-scheme RC kernel (ablation)   // WS_LUT_GLOBAL=1: read the LUT pool through L1 instead of staging it

@@ -2882,6 +2882,42 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         if (lse) la.persistent<true, true>(s, w, g, kind);
         else la.persistent<false, false>(s, w, g, kind);
         if (lse && (flags & WS_RUN_CORNER_SUM)) la.corner_sum(s);
+    } else if (fused && !bwd_done && !(flags & WS_RUN_TIMED) && gs && ctx.split_min > 0 &&
+               nc >= ctx.split_min) {
+        // large corner batches: two half batches as independent fused passes
+        // on the two streams, so one half's level-boundary gaps (PDL release,
+        // the last wave) fill with the other's blocks; the batch gradient sum
+        // runs after the join over all corners in corner order (bitwise the
+        // lockstep batch)
+        std::vector<cudaEvent_t>& ev = ctx.events;
+        while ((int)ev.size() < 2) {
+            cudaEvent_t e;
+            WS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+        }
+        WS_CUDA(cudaEventRecord(ev[0], s));   // fork
+        WS_CUDA(cudaStreamWaitEvent(gs, ev[0], 0));
+        const int h = nc / 2;
+        Launcher lh[2] = {Launcher(ctx, c0, h), Launcher(ctx, c0 + h, nc - h)};
+        const cudaStream_t st[2] = {s, gs};
+        for (int x = 0; x < 2; x++)
+            if (!lh[x].rc(st[x], w, true, true)) lh[x].free_pins(st[x], true);
+        for (int li = 0; li < L; li++)
+            for (int x = 0; x < 2; x++) lh[x].fwd<true, true>(st[x], li, g);
+        for (int x = 0; x < 2; x++) {
+            lh[x].pg = pg_fused;
+            if (pg_fused) posgrad_reset(ctx, lh[x].c0, lh[x].nc, st[x]);
+        }
+        for (int li = L - 1; li >= 0; li--)
+            for (int x = 0; x < 2; x++) lh[x].bwd<true, true>(st[x], li, g, kind);
+        for (int x = 0; x < 2; x++) {
+            lh[x].fin_summary(st[x], g, kind);
+            if (pg_fused) lh[x].count += launch_posgrad_tail(ctx, lh[x].c0, lh[x].nc, st[x], true);
+        }
+        WS_CUDA(cudaEventRecord(ev[1], gs));  // join
+        WS_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
+        la.count += lh[0].count + lh[1].count;
+        if (flags & WS_RUN_CORNER_SUM) la.corner_sum(s);
     } else if (fused) {
         // WS_RUN_TIMED: kinds 0 RC, 1 fused forward+LSE level, 2 fused
         // backward+gradient level, 5 tail (the events serialise the PDL overlap)

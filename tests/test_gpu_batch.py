@@ -77,3 +77,44 @@ def test_batch_graph_replay_c1():
         dev.run(FUSED | _lib.RUN_CORNER_SUM | _lib.RUN_GRAPH, corner=0, n_corners=16)
     assert np.array_equal(dev.get("d_arc_sum"), ref[0]) and np.array_equal(dev.get("arrival", 15), ref[1])
     dev.close()
+
+
+def _with_env(var, val, fn):
+    import os
+    old = os.environ.get(var)
+    os.environ[var] = val
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[var]
+        else:
+            os.environ[var] = old
+
+
+@pytest.mark.parametrize("nc", [5, 8, 16])
+def test_batch_split_streams_bitwise(nc):
+    """Fused batches of >= WS_SPLIT corners run as two half batches on the
+    context's two streams (the default for >= 8); every field, the summaries
+    and the batch gradient sum equal the lockstep batch (WS_SPLIT=0)."""
+    raw = raw_of(load("gen_heavy_1500"))
+
+    def run(split):
+        def go():
+            dev = ws.DeviceDesign(raw, n_corners=nc)
+            for k in range(nc):
+                dev.set_values(k, **corner_values(raw, k))
+            for _ in range(2):     # the second run replays the captured graph
+                dev.run(FUSED | _lib.RUN_GRAPH | _lib.RUN_CORNER_SUM, corner=0, n_corners=nc)
+            out = [{f: dev.get(f, k) for f in ST_FIELDS + G_FIELDS} for k in range(nc)]
+            out.append({f: dev.get(f) for f in ("d_arc_sum", "d_edge_sum")})
+            out.append([dev.summary(k) for k in range(nc)])
+            dev.close()
+            return out
+        return _with_env("WS_SPLIT", split, go)
+
+    a, b = run("0"), run("4")
+    for k in range(nc + 1):
+        for f in a[k]:
+            assert np.array_equal(a[k][f], b[k][f], equal_nan=True), (k, f)
+    assert a[-1] == b[-1]

@@ -278,3 +278,35 @@ def test_place_candidate_batch_bitwise_single(nc):
         for f, _ in PG_FIELDS:
             assert np.array_equal(dev.get(f, k), batch[k][f], equal_nan=True), (k, f)
     dev.close()
+
+
+def test_place_candidate_batch_split_streams_bitwise():
+    """Placement-candidate batches of >= WS_SPLIT candidates run as two half
+    batches on two streams (fused sweep included): bitwise the lockstep
+    batch (WS_SPLIT=0)."""
+    import os
+    raw = _sweep_case("big_star")
+    nc = 8
+    pls = [PL.synthetic_placement(raw, seed=40 + k) for k in range(nc)]
+
+    def run(split):
+        old = os.environ.get("WS_SPLIT")
+        os.environ["WS_SPLIT"] = split
+        try:
+            dev = ws.DeviceDesign(raw, n_corners=nc)
+        finally:
+            if old is None:
+                del os.environ["WS_SPLIT"]
+            else:
+                os.environ["WS_SPLIT"] = old
+        timers = [PL.PlacementTimer(dev, pls[k], corner=k, graph=False) for k in range(nc)]
+        dev.run(PL.PlacementTimer.FLAGS, corner=0, n_corners=nc)
+        out = [{f: dev.get(f, k) for f, _ in PG_FIELDS} for k in range(nc)]
+        dev.close()
+        del timers
+        return out
+
+    a, b = run("0"), run("4")
+    for k in range(nc):
+        for f, _ in PG_FIELDS:
+            assert np.array_equal(a[k][f], b[k][f], equal_nan=True), (k, f)
