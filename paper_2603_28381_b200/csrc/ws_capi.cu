@@ -286,6 +286,8 @@ int ws_create(const ws_design_desc* d, int n_corners, ws_ctx** out)
             c.rc_pin_order = r && std::string(r) == "pin";
             const char* sp = getenv("WS_SPLIT");
             c.split_min = sp ? atoi(sp) : 8;   // measured: 16 corners 11.21 -> 10.56 ms, 8 corners 5.83 -> 5.28 ms
+            const char* spp = getenv("WS_SPLIT_PARTS");
+            c.split_parts = spp ? atoi(spp) : 2;
             const char* rr = getenv("WS_RC_ROOTS");
             c.rc_roots = !rr ? 0 : std::string(rr) == "net" ? -1 : std::string(rr) == "fold" ? 1 : 0;
         }
@@ -328,6 +330,7 @@ void ws_destroy(ws_ctx* h)
     c.scratch.release();
     if (c.s_main) cudaStreamDestroy(c.s_main);
     if (c.s_grad) cudaStreamDestroy(c.s_grad);
+    for (cudaStream_t x : c.split_streams) cudaStreamDestroy(x);
     delete h;
 }
 

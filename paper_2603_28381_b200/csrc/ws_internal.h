@@ -150,6 +150,8 @@ struct Context {
     SumPlan* tns_plan = nullptr;      // over 2E slack terms
     int launches_last_run = 0;
     bool lut_global = false;
+    int split_parts = 2;         // WS_SPLIT_PARTS: streams a split batch runs on (parts of >= 4 corners)
+    std::vector<cudaStream_t> split_streams;   // the parts beyond s_main / s_grad
     int split_min = 8;           // WS_SPLIT=n: fused corner batches of >= n corners run as two half batches on two streams (0: never)
     int rc_roots = 0;            // WS_RC_ROOTS: star-net root loads in net blocks (net, -1) / member blocks (fold, 1) / by batch size (0)
     bool rc_pin_order = false;   // WS_RC_SCHEME=pin: the pin-order streaming RC

@@ -2889,34 +2889,50 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         // the last wave) fill with the other's blocks; the batch gradient sum
         // runs after the join over all corners in corner order (bitwise the
         // lockstep batch)
+        // parts: WS_SPLIT_PARTS (default 2), each part >= 4 corners
+        const int parts = std::max(2, std::min(std::min(ctx.split_parts, nc / 4), 8));
         std::vector<cudaEvent_t>& ev = ctx.events;
-        while ((int)ev.size() < 2) {
+        while ((int)ev.size() < 1 + parts) {
             cudaEvent_t e;
             WS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             ev.push_back(e);
         }
+        while ((int)ctx.split_streams.size() < parts - 2) {
+            cudaStream_t x;
+            WS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            ctx.split_streams.push_back(x);
+        }
+        std::vector<cudaStream_t> st(parts);
+        st[0] = s;
+        st[1] = gs;
+        for (int x = 2; x < parts; x++) st[x] = ctx.split_streams[x - 2];
         WS_CUDA(cudaEventRecord(ev[0], s));   // fork
-        WS_CUDA(cudaStreamWaitEvent(gs, ev[0], 0));
-        const int h = nc / 2;
-        Launcher lh[2] = {Launcher(ctx, c0, h), Launcher(ctx, c0 + h, nc - h)};
-        const cudaStream_t st[2] = {s, gs};
-        for (int x = 0; x < 2; x++)
+        for (int x = 1; x < parts; x++) WS_CUDA(cudaStreamWaitEvent(st[x], ev[0], 0));
+        std::vector<Launcher> lh;
+        lh.reserve(parts);
+        for (int x = 0; x < parts; x++) {
+            const int a = nc * x / parts, b = nc * (x + 1) / parts;
+            lh.emplace_back(ctx, c0 + a, b - a);
+        }
+        for (int x = 0; x < parts; x++)
             if (!lh[x].rc(st[x], w, true, true)) lh[x].free_pins(st[x], true);
         for (int li = 0; li < L; li++)
-            for (int x = 0; x < 2; x++) lh[x].fwd<true, true>(st[x], li, g);
-        for (int x = 0; x < 2; x++) {
+            for (int x = 0; x < parts; x++) lh[x].fwd<true, true>(st[x], li, g);
+        for (int x = 0; x < parts; x++) {
             lh[x].pg = pg_fused;
             if (pg_fused) posgrad_reset(ctx, lh[x].c0, lh[x].nc, st[x]);
         }
         for (int li = L - 1; li >= 0; li--)
-            for (int x = 0; x < 2; x++) lh[x].bwd<true, true>(st[x], li, g, kind);
-        for (int x = 0; x < 2; x++) {
+            for (int x = 0; x < parts; x++) lh[x].bwd<true, true>(st[x], li, g, kind);
+        for (int x = 0; x < parts; x++) {
             lh[x].fin_summary(st[x], g, kind);
             if (pg_fused) lh[x].count += launch_posgrad_tail(ctx, lh[x].c0, lh[x].nc, st[x], true);
         }
-        WS_CUDA(cudaEventRecord(ev[1], gs));  // join
-        WS_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
-        la.count += lh[0].count + lh[1].count;
+        for (int x = 1; x < parts; x++) {     // join
+            WS_CUDA(cudaEventRecord(ev[x], st[x]));
+            WS_CUDA(cudaStreamWaitEvent(s, ev[x], 0));
+        }
+        for (int x = 0; x < parts; x++) la.count += lh[x].count;
         if (flags & WS_RUN_CORNER_SUM) la.corner_sum(s);
     } else if (fused) {
         // WS_RUN_TIMED: kinds 0 RC, 1 fused forward+LSE level, 2 fused
