@@ -36,6 +36,30 @@ for topo in ("star", "random_tree"):
     assert np.array_equal(a, dev.get("d_xy", 1))
     print(topo, dev.summary(), float(np.abs(timer.grad_xy()).max()))
     dev.close()
+# corner batches: 8 corners in the fused mode = two half batches on two
+# streams (the split), the batch level kernels, star-net root loads folded
+# in the RC member blocks, the in-kernel corner sum; then 8 placement
+# candidates (fused sweep, split) — bitwise against the lockstep batch
+from paper_2603_28381_b200.corners import corner_values
+raw = G.generate_raw(G.GeneratorConfig(num_cells=600, fanout=G.power_law(2.0, 150), depth_target=6, seed=5))
+outs = []
+for split in ("8", "0"):
+    os.environ["WS_SPLIT"] = split
+    dev = ws.DeviceDesign(raw, n_corners=8)
+    del os.environ["WS_SPLIT"]
+    for k in range(8):
+        dev.set_values(k, **corner_values(raw, k))
+    dev.run(_lib.RUN_HARD | _lib.RUN_LSE | _lib.RUN_GRAD | _lib.RUN_FUSED | _lib.RUN_CORNER_SUM, corner=0,
+            n_corners=8)
+    o = [dev.get("d_arc_sum")] + [dev.get("adjoint", k) for k in range(8)]
+    timers = [PL.PlacementTimer(dev, PL.synthetic_placement(raw, seed=30 + k), corner=k, graph=False)
+              for k in range(8)]
+    dev.run(PL.PlacementTimer.FLAGS, corner=0, n_corners=8)
+    o += [dev.get("d_xy", k) for k in range(8)]
+    outs.append(o)
+    dev.close()
+assert all(np.array_equal(x, y) for x, y in zip(*outs))
+print("batch split ok")
 d = tempfile.mkdtemp()
 ws.save_raw(os.path.join(d, "x.npz"), raw)
 dev = ws.DeviceDesign.from_file(os.path.join(d, "x.npz"))
