@@ -371,8 +371,11 @@ def corner_batch(raw, rank, world, steps, flush, dist=None, n_total=16):
         stream.wait_event(done[b])                 # reduce buffer b free again
         dev.run(flags, corner=0, n_corners=nc, stream=stream)
         ra, re, rs = red[b]
-        ra.copy_(dsum[0])
-        re.copy_(dsum[1])
+        if dist is not None:
+            # double-buffered for the exchange overlapped with the next
+            # batch (one GPU: nothing to exchange, the sums stay in place)
+            ra.copy_(dsum[0])
+            re.copy_(dsum[1])
         rs.copy_(combine_local(summ))
         ready[b].record(stream)
         if dist is not None:
