@@ -47,6 +47,9 @@ namespace ws {
 #ifndef WS_MINB
 #define WS_MINB 2   // min resident blocks per SM of the level kernels
 #endif
+#ifndef WS_MINB_PG_BATCH
+#define WS_MINB_PG_BATCH 3   // ... of the fused position-gradient backward level kernel in batches (>= 4 slots)
+#endif
 #ifndef WS_MINB_BATCH
 #define WS_MINB_BATCH 4   // ... of the fused level kernels in corner batches (>= 4 corners)
 #endif
@@ -2743,10 +2746,16 @@ struct Launcher {
         if (nt <= 0) return;
         const int variant = H && G ? 3 : (H ? 1 : 2);
         const PgDev pd = pg ? pg_dev(ctx, c0) : PgDev{nullptr, nullptr, nullptr};
-        if (H && G && pg)
-            launch(k_bwd<H, G, WS_MINB, true>, dim3(nt, nc), dim3(PASS_TPB), pg_smem_bytes(), s, probed(nt),
-                   cs, ctx.lvt_ptr_host[li], g, kind, variant, ls, use_smem, pd, pg_off());
-        else if (H && G && nc >= 4)
+        if (H && G && pg) {
+            // candidate batches: 3 blocks/SM (80 registers; 16 candidates
+            // 18.62 -> 18.14 ms); one candidate keeps 2 (1.48 vs 1.65 ms)
+            if (nc >= 4)
+                launch(k_bwd<H, G, WS_MINB_PG_BATCH, true>, dim3(nt, nc), dim3(PASS_TPB), pg_smem_bytes(), s,
+                       probed(nt), cs, ctx.lvt_ptr_host[li], g, kind, variant, ls, use_smem, pd, pg_off());
+            else
+                launch(k_bwd<H, G, WS_MINB, true>, dim3(nt, nc), dim3(PASS_TPB), pg_smem_bytes(), s, probed(nt),
+                       cs, ctx.lvt_ptr_host[li], g, kind, variant, ls, use_smem, pd, pg_off());
+        } else if (H && G && nc >= 4)
             launch(k_bwd<H, G, WS_MINB_BATCH>, dim3(nt, nc), dim3(PASS_TPB), 0, s, probed(nt), cs,
                    ctx.lvt_ptr_host[li], g, kind, variant, ls, false, pd, 0);
         else
@@ -2869,9 +2878,12 @@ void run_chunk(Context& ctx, int c0, int nc, unsigned flags, double g, int kind,
         WS_CUDA(cudaFuncSetAttribute(k_fwd<true, true, WS_MINB_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)la.lut_bytes));
     }
-    if (pg_fused)   // the staged pool + the sweep's per-task state exceed the default 48 KB
+    if (pg_fused) {   // the staged pool + the sweep's per-task state exceed the default 48 KB
         WS_CUDA(cudaFuncSetAttribute(k_bwd<true, true, WS_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)la.pg_smem_bytes()));
+        WS_CUDA(cudaFuncSetAttribute(k_bwd<true, true, WS_MINB_PG_BATCH, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la.pg_smem_bytes()));
+    }
     const bool hard = flags & WS_RUN_HARD, lse = flags & WS_RUN_LSE, grad = flags & WS_RUN_GRAD;
     const bool fused = (flags & WS_RUN_FUSED) && hard && lse && grad;
     const bool two = (flags & WS_RUN_TWO_STREAM) && hard && (lse || grad) && !fused;
