@@ -950,12 +950,6 @@ void build_topology(Context& ctx, const ws_design_desc* d)
                                                   t.root_net_of_pin, t.rc_code);
         WS_CHECK_LAUNCH();
     }
-    {
-        const int nb = (M + RC_MPB - 1) / RC_MPB;
-        t.rc_bnet = ar.alloc<int>(nb + 1);
-        k_rc_bnet<<<blocks_for(nb + 1), TPB, 0, s>>>(nb, N, t.net_ptr, t.rc_bnet);
-        WS_CHECK_LAUNCH();
-    }
     t.rc_pcode = ar.alloc<int>(P);
     if (P) {
         k_rc_pcode<<<blocks_for(P), TPB, 0, s>>>(P, t.member_of_pin, t.root_net_of_pin, t.mem_net,
@@ -986,6 +980,14 @@ void build_topology(Context& ctx, const ws_design_desc* d)
     }
 
     build_tasks(ctx);
+    {
+        // last in the arena: the batch-only RC owner table leaves the
+        // addresses of everything the single-corner pass reads unchanged
+        const int nb = (M + RC_MPB - 1) / RC_MPB;
+        ctx.rc_bnet = ar.alloc<int>(nb + 1);
+        k_rc_bnet<<<blocks_for(nb + 1), TPB, 0, s>>>(nb, N, t.net_ptr, ctx.rc_bnet);
+        WS_CHECK_LAUNCH();
+    }
     WS_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -50,7 +50,6 @@ struct Topo {
     int *net_tree;                   // 1 if any member has a non-root parent
     int *rc_code;                    // per member: -1 (tree net) or pin << 1 | (pin is a root)
     int *rc_pcode;                   // per pin: the pin-order RC code (ws_build.cu k_rc_pcode)
-    int *rc_bnet;                    // per streaming-RC member block b (+1): first net whose members start at or after b * RC_MPB
     int *pin_ep_ptr, *pin_ep_idx;    // endpoint entries grouped by pin (stable)
     int *pin_pi;                     // pin -> PI index or -1
     int *pin_out_ptr, *pin_out_arc;  // arcs grouped by source pin (all pins)

@@ -150,6 +150,7 @@ struct Context {
     SumPlan* tns_plan = nullptr;      // over 2E slack terms
     int launches_last_run = 0;
     bool lut_global = false;
+    int* rc_bnet = nullptr;      // per streaming-RC member block b (+1): first net whose members start at or after b * RC_MPB (k_rc_flat<true>; kept out of Topo so the level kernels' parameters stay put)
     int split_parts = 2;         // WS_SPLIT_PARTS: streams a split batch runs on (parts of >= 4 corners)
     std::vector<cudaStream_t> split_streams;   // the parts beyond s_main / s_grad
     int split_min = 8;           // WS_SPLIT=n: fused corner batches of >= n corners run as two half batches on two streams (0: never)

@@ -1421,8 +1421,11 @@ constexpr int RC_TPB = 256, RC_ITEMS = 4;
 // (member, cond): the member's res / cap are gathered (32 B per pin) and the
 // pin's load / net_delay / impulse rows are written contiguously (full
 // lines), the non-member roots' zero delay / impulse included.
+// FOLD (corner batches): no net blocks (nbn == 0); the member blocks fold
+// the star-net root loads.  The single-corner instance has no shared memory.
+template <bool FOLD>
 __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm, int nbn, int nbf,
-                                                    bool lse, bool pin_order)
+                                                    bool lse, bool pin_order, const int* __restrict__ bnet)
 {
     pdl_trigger();
     const Corner& C = cs.c[blockIdx.y];
@@ -1501,7 +1504,7 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm,
             C.net_delay[pin * 4 + c] = d;
             C.impulse[pin * 4 + c] = rad > 0.0 ? __dsqrt_rn(rad) : 0.0;
         }
-        if (nbn == 0) {
+        if (FOLD) {
             // root loads of the star nets whose members start in this block
             // (no separate net blocks): the block's caps from shared memory,
             // a net running past the block's end from global; the same
@@ -1511,7 +1514,7 @@ __global__ void __launch_bounds__(RC_TPB) k_rc_flat(Topo t, Corners cs, int nbm,
 #pragma unroll
             for (int k = 0; k < RC_ITEMS; k++) sc[threadIdx.x + k * RC_TPB] = b[k];
             __syncthreads();
-            const int n0 = LDG(t.rc_bnet + bx), n1 = LDG(t.rc_bnet + bx + 1);
+            const int n0 = LDG(bnet + bx), n1 = LDG(bnet + bx + 1);
             for (int x = threadIdx.x; x < (n1 - n0) * 4; x += RC_TPB) {
                 const int n = n0 + (x >> 2), c = x & 3;
                 if (LDG(t.net_tree + n)) continue;       // k_rc_tree
@@ -2698,8 +2701,9 @@ struct Launcher {
             if (ctx.rc_cte)
                 launch(k_rc_cte, dim3((ctx.t.N + CTE_NETS - 1) / CTE_NETS, nc), dim3(CTE_NETS), 0, s, ctx.t, cs);
             else
-                launch(k_rc_flat, dim3(nbm + nbn_flat + nbf, nc), dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn_flat, nbf, lse,
-                       po);
+                launch(fold_in_members ? k_rc_flat<true> : k_rc_flat<false>, dim3(nbm + nbn_flat + nbf, nc),
+                       dim3(RC_TPB), 0, s, ctx.t, cs, nbm, nbn_flat, nbf, lse, po,
+                       (const int*)ctx.rc_bnet);
             if (ctx.any_tree) {
                 count++;
                 launch(k_rc_tree, dim3(nbn, nc), dim3(RC_TPB), 0, s, ctx.t, cs);
